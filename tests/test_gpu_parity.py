@@ -1,0 +1,390 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the FP64 oracle.
+
+Bars (stated here and in DESIGN.md):
+  * indices (DeMo frequency indices, Random/Striding sets, payload layout): bit-exact;
+  * sign-mode / ternary wire values: exact;
+  * FP32 values (coefficients, local_q, m, Q, p, Adam moments) against the FP64 oracle
+    fed the same FP32 inputs: |gpu - oracle| <= TOL * scale, TOL = 1e-5, scale = the
+    L-inf of the oracle quantity over the chunk (norm-relative per chunk, so a
+    cancellation inside a chunk cannot fake a failure);
+  * fp16 wire values: within one binary16 ulp of the oracle's (the GPU rounds an FP32
+    coefficient, the oracle an FP64 one).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.oracle import DEMO, DILOCO, FP16, FP32, FULL, RANDOM, STRIDING, TERNARY, Rep
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def P():
+    import paper_2502_06728_b200 as mod
+
+    return mod
+
+
+def dev(x):
+    return torch.as_tensor(np.asarray(x, np.float32)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def rep_to_cfg(rep: Rep):
+    p = P()
+    return p.ReplicatorConfig(p.Scheme(rep.scheme), rep.chunk_size, rep.top_k, rep.compression, rep.sign_mode,
+                              p.TransferDtype(rep.transfer_dtype), rep.seed)
+
+
+def chunk_close(got, want, s, tol=TOL, what=""):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    assert got.shape == want.shape, (what, got.shape, want.shape)
+    n = len(want)
+    pad = (-n) % s
+    g = np.concatenate([got, np.zeros(pad)]).reshape(-1, s)
+    w = np.concatenate([want, np.zeros(pad)]).reshape(-1, s)
+    scale = np.maximum(np.abs(w).max(axis=1), 1e-30)
+    err = np.abs(g - w).max(axis=1) / scale
+    bad = np.nonzero(err > tol)[0]
+    assert len(bad) == 0, f"{what}: {len(bad)} chunks over tol, worst {err.max():.3g} at chunk {bad[:5]}"
+
+
+def fp16_close(got, want):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    ulp = np.maximum(np.abs(want), 2.0**-14) * 2.0**-10
+    assert np.all(np.abs(got - want) <= ulp * 1.0001), np.abs(got - want).max()
+
+
+def check_values(got, want, rep: Rep, group):
+    if rep.sign_mode or rep.transfer_dtype == TERNARY:
+        assert np.array_equal(got, want)
+    elif rep.transfer_dtype == FP16:
+        fp16_close(got, want)
+    else:
+        chunk_close(got, want, group, what="values")
+
+
+# --------------------------------------------------------------- transform / encode
+def test_demo_extraction_matches_golden(golden):
+    p = P()
+    g = golden["transform"]
+    for ci in range(10):
+        s, k, n = (int(x) for x in g[f"x_{ci}"])
+        rep = Rep(scheme=DEMO, chunk_size=s, top_k=k, compression=k / s, sign_mode=False)
+        enc = p.select_and_encode(dev(g[f"v_{ci}"]), rep_to_cfg(rep), 0, 0)
+        idx = enc.update.freq_indices.cpu().numpy().astype(np.uint32)
+        assert np.array_equal(idx, g[f"idx_{ci}"]), f"case {ci} (s={s} k={k}) indices differ"
+        chunk_close(host(enc.update.values), g[f"co_{ci}"], k, what=f"coeffs {ci}")
+        chunk_close(host(enc.local_q), g[f"fast_{ci}"], s, what=f"fast {ci}")
+        if k == s:  # full band: exact identity (transform.cpp:119-125)
+            assert np.array_equal(host(enc.local_q), g[f"v_{ci}"])
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("s,k", [(64, 32), (64, 8), (64, 56), (32, 4), (16, 5), (128, 16), (64, 1), (7, 3)])
+def test_demo_indices_bit_exact_random(oracle, seed, s, k):
+    p = P()
+    rng = np.random.default_rng(1000 * seed + s + k)
+    n = 64 * 257 + 13
+    v = rng.standard_normal(n).astype(np.float32)
+    # tie and degenerate chunks
+    v[:64] = 0.0
+    v[64:128] = 0.5
+    v[128:192] = np.tile(v[192:200], 8)
+    v[256:320] *= 1e-30
+    for sign in (False, True):
+        rep = Rep(scheme=DEMO, chunk_size=s, top_k=k, compression=k / s, sign_mode=sign)
+        want = oracle.select_and_encode(v.astype(np.float64), rep, 3, 1)
+        enc = p.select_and_encode(dev(v), rep_to_cfg(rep), 3, 1)
+        got_idx = enc.update.freq_indices.cpu().numpy().astype(np.uint32)
+        assert np.array_equal(got_idx, want["freq_indices"])
+        check_values(host(enc.update.values), want["values"], rep, k)
+        chunk_close(host(enc.local_q), want["local_q"], s, what="local_q")
+        assert enc.update.bytes == want["bytes"]
+
+
+def test_demo_large_config1_indices(oracle):
+    """config-1 flavour at 2^20 elements: s=64, k=32, sign on; every index bit-exact"""
+    p = P()
+    n = 1 << 20
+    v = (np.random.default_rng(7).standard_normal(n) * 1e-3).astype(np.float32)
+    rep = Rep(scheme=DEMO, chunk_size=64, top_k=32, compression=0.5, sign_mode=True)
+    want = oracle.select_and_encode(v.astype(np.float64), rep, 0, 0)
+    enc = p.select_and_encode(dev(v), rep_to_cfg(rep), 0, 0)
+    assert np.array_equal(enc.update.freq_indices.cpu().numpy().astype(np.uint32), want["freq_indices"])
+    assert np.array_equal(host(enc.update.values), want["values"])
+    chunk_close(host(enc.local_q), want["local_q"], 64, what="local_q")
+
+
+def test_golden_replicate_all_schemes(golden):
+    p = P()
+    g = golden["replicate"]
+    for ci in range(int(g["count"][0])):
+        scheme, dtype, sign, step, s, k = (int(x) for x in g[f"cfg_{ci}"])
+        rep = Rep(scheme=scheme, chunk_size=s, top_k=k, sign_mode=bool(sign), transfer_dtype=dtype,
+                  compression=1.0 if scheme == FULL else 0.25, seed=99)
+        cfg = rep_to_cfg(rep)
+        ups = []
+        for r in range(3):
+            v = g[f"v_{ci}_{r}"]
+            enc = p.select_and_encode(dev(v), cfg, step, 2)
+            meta = [int(x) for x in g[f"meta_{ci}_{r}"]]
+            assert [enc.update.bytes, int(enc.update.empty)] == meta, (ci, r)
+            if scheme == DEMO:
+                assert np.array_equal(enc.update.freq_indices.cpu().numpy().astype(np.uint32),
+                                      g[f"freq_indices_{ci}_{r}"]), (ci, r)
+            group = k if scheme == DEMO else max(len(g[f"values_{ci}_{r}"]), 1)
+            if len(g[f"values_{ci}_{r}"]):
+                check_values(host(enc.update.values), g[f"values_{ci}_{r}"], rep, group)
+            chunk_close(host(enc.local_q), g[f"local_q_{ci}_{r}"], s if scheme == DEMO else len(v),
+                        what=f"local_q {ci}")
+            ups.append(enc.update)
+        if f"q_{ci}_R1" in g:
+            for R in (1, 2, 3):
+                q = p.decode_and_merge(ups[:R], cfg)
+                want = g[f"q_{ci}_R{R}"]
+                if rep.transfer_dtype == FP16 and not rep.sign_mode:
+                    chunk_close(host(q), want, s if scheme == DEMO else len(want), tol=2e-3, what=f"q {ci}")
+                else:
+                    chunk_close(host(q), want, s if scheme == DEMO else len(want), what=f"q {ci} R{R}")
+            wire = np.frombuffer(p.serialize(ups[0], p.TransferDtype(dtype)), np.uint8)
+            ref = g[f"wire_{ci}"]
+            assert len(wire) == len(ref) and np.array_equal(wire[:9], ref[:9])
+            if rep.sign_mode or dtype == TERNARY or scheme != DEMO:
+                assert np.array_equal(wire, ref), ci
+            if scheme == DEMO:  # indices part of the body is bit-exact
+                ni = int(len(g[f"freq_indices_{ci}_0"])) * 4
+                assert np.array_equal(wire[9:9 + ni], ref[9:9 + ni])
+
+
+def test_random_index_sets_bit_exact(golden):
+    p = P()
+    g = golden["replicate"]
+    for j in range(5):
+        L, step, shard, seed = (int(x) for x in g[f"rand_cfg_{j}"])
+        cfg = p.ReplicatorConfig(p.Scheme.Random, compression=float(g[f"rand_c_{j}"][0]), seed=seed)
+        got = p.selected_indices(cfg, step, shard, L).cpu().numpy()
+        assert np.array_equal(got, g[f"rand_idx_{j}"].astype(np.int64)), j
+
+
+@pytest.mark.parametrize("L,c", [(1000, 0.25), (21468, 1 / 8), (300001, 1 / 16), (4096, 1.0), (777, 0.5)])
+def test_random_index_sets_vs_oracle(oracle, L, c):
+    p = P()
+    for step in (0, 1, 9):
+        for shard in (0, 3):
+            rep = Rep(scheme=RANDOM, compression=c, seed=1234)
+            want = oracle.selected_indices(rep, step, shard, L)
+            got = p.selected_indices(rep_to_cfg(rep), step, shard, L).cpu().numpy()
+            assert np.array_equal(got, want.astype(np.int64)), (step, shard)
+
+
+def test_striding_sets(oracle):
+    p = P()
+    for L, c in ((10, 0.25), (1000, 1 / 7), (65, 0.5)):
+        for step in range(6):
+            rep = Rep(scheme=STRIDING, compression=c)
+            got = p.selected_indices(rep_to_cfg(rep), step, 0, L).cpu().numpy()
+            assert np.array_equal(got, oracle.selected_indices(rep, step, 0, L).astype(np.int64))
+
+
+# --------------------------------------------------------------- optimizer stages
+@pytest.mark.parametrize("scheme", [DEMO, RANDOM, STRIDING, DILOCO, FULL])
+def test_sgd_stage_parity(oracle, scheme):
+    """Stage parity: each step the oracle is fed the GPU's FP32 state."""
+    p = P()
+    n = 64 * 64 + 29
+    rep = Rep(scheme=scheme, chunk_size=64, top_k=32, compression=1.0 if scheme == FULL else 0.25,
+              sign_mode=True, seed=1234)
+    cfg = rep_to_cfg(rep)
+    opt = p.OptimizerConfig(momentum_decay=0.9)
+    st = p.MomentumState.make(p.OptimizerKind.DemoSgd, n)
+    params = dev(np.random.default_rng(1).standard_normal(n) * 0.02)
+    for step in range(5):
+        g = (np.random.default_rng(100 + step).standard_normal(n) * 1e-3).astype(np.float32)
+        m_in = host(st.m)
+        p_in = host(params)
+        tr = p.StepTrace()
+        enc = p.demo_sgd_prepare(st, dev(g), opt, cfg, step, 0, tr)
+        m_o = m_in.copy()
+        want = oracle.demo_sgd_prepare(m_o, g.astype(np.float64), 0.9, rep, step, 0)
+        chunk_close(host(tr.m_accum), want["m_accum"], 64, what="m_accum")
+        # selection is checked on the GPU's own accumulated momentum
+        again = oracle.select_and_encode(host(tr.m_accum), rep, step, 0)
+        if scheme == DEMO:
+            assert np.array_equal(enc.update.freq_indices.cpu().numpy().astype(np.uint32), again["freq_indices"])
+        assert enc.update.empty == again["empty"] and enc.update.bytes == again["bytes"]
+        if not again["empty"]:
+            assert np.array_equal(host(enc.update.values), again["values"])
+        chunk_close(host(tr.local_q), again["local_q"], 64, what="local_q")
+        chunk_close(host(st.m), host(tr.m_accum) - again["local_q"], 64, what="m_after")
+        # merge + apply
+        if not enc.update.empty:
+            q = p.decode_and_merge([enc.update], cfg)
+            want_q = oracle.decode_and_merge(rep, [again["values"]], [again["freq_indices"]], n, step, 0)
+            chunk_close(host(q), want_q, 64, what="Q")
+            p.demo_sgd_apply(params, q, 0.01)
+            p_want = p_in.copy()
+            oracle.demo_sgd_apply(p_want, want_q, 0.01)
+        else:
+            p.demo_sgd_apply(params, dev(g), 0.01)
+            p_want = p_in - 0.01 * g.astype(np.float64)
+        chunk_close(host(params), p_want, 64, what="params")
+
+
+def test_conservation_exact_form():
+    """acceptance 03 / test_optim.cpp:76-96: m_after == m_accum - local_q elementwise"""
+    p = P()
+    n = 96 * 64
+    for sign in (False, True):
+        cfg = p.ReplicatorConfig(p.Scheme.DeMo, 64, 8, 8 / 64, sign)
+        st = p.MomentumState.make(p.OptimizerKind.DemoSgd, n)
+        for step in range(4):
+            tr = p.StepTrace()
+            p.demo_sgd_prepare(st, torch.randn(n, device="cuda"), p.OptimizerConfig(), cfg, step, 0, tr)
+            assert torch.equal(tr.m_after, tr.m_accum - tr.local_q)
+
+
+def test_full_band_flushes_to_zero():
+    """test_optim.cpp:121-134: k == s takes everything, m becomes exactly 0"""
+    p = P()
+    n = 64 * 10
+    st = p.MomentumState.make(p.OptimizerKind.DemoSgd, n)
+    p.demo_sgd_prepare(st, torch.randn(n, device="cuda"), p.OptimizerConfig(), p.ReplicatorConfig(p.Scheme.DeMo, 32, 4, sign_mode=False), 0, 0)
+    tr = p.StepTrace()
+    p.demo_sgd_prepare(st, torch.randn(n, device="cuda"), p.OptimizerConfig(),
+                       p.ReplicatorConfig(p.Scheme.DeMo, 32, 32, sign_mode=False), 1, 0, tr)
+    assert torch.equal(tr.local_q, tr.m_accum)
+    assert torch.count_nonzero(st.m) == 0
+
+
+def test_single_replica_merge_reproduces_local_share():
+    """test_replicate.cpp:305-311 (within FP32 tolerance; bitwise in the reference's FP64)"""
+    p = P()
+    v = torch.randn(96 * 10, device="cuda")
+    cfg = p.ReplicatorConfig(p.Scheme.DeMo, 32, 4, sign_mode=False)
+    enc = p.select_and_encode(v, cfg, 0, 0)
+    q = p.decode_and_merge([enc.update], cfg)
+    chunk_close(host(q), host(enc.local_q), 32, tol=1e-6, what="single merge")
+
+
+def test_adamw_stage_parity(oracle):
+    p = P()
+    n = 64 * 40 + 5
+    rep = Rep(scheme=DEMO, chunk_size=64, top_k=16, compression=0.25, sign_mode=True, seed=1234)
+    cfg = rep_to_cfg(rep)
+    opt = p.OptimizerConfig(p.OptimizerKind.DecoupledAdamW, weight_decay=0.01)
+    st = p.MomentumState.make(p.OptimizerKind.DecoupledAdamW, n)
+    params = dev(np.random.default_rng(2).standard_normal(n) * 0.02)
+    for step in range(4):
+        g = (np.random.default_rng(200 + step).standard_normal(n) * 1e-3).astype(np.float32)
+        p_in, ea_in, es_in = host(params), host(st.exp_avg), host(st.exp_avg_sq)
+        enc = p.adamw_prepare(dev(g), cfg, step, 0)
+        want = oracle.select_and_encode(g.astype(np.float64), rep, step, 0)
+        assert np.array_equal(enc.update.freq_indices.cpu().numpy().astype(np.uint32), want["freq_indices"])
+        q = p.decode_and_merge([enc.update], cfg)
+        p.adamw_apply(params, st, dev(g), enc.local_q, q, opt, 0.003)
+        want_q = oracle.decode_and_merge(rep, [want["values"]], [want["freq_indices"]], n, step, 0)
+        pw, ew, sw = p_in.copy(), ea_in.copy(), es_in.copy()
+        oracle.adamw_apply(pw, ew, sw, step, g.astype(np.float64), want["local_q"], want_q, 0.9, 0.999, 1e-8,
+                           0.01, 0.003)
+        chunk_close(host(st.exp_avg), ew, 64, tol=1e-4, what="exp_avg")
+        chunk_close(host(st.exp_avg_sq), sw, 64, tol=1e-4, what="exp_avg_sq")
+        # p moves by ~lr per step: compare the update, relative to lr
+        assert np.abs(host(params) - pw).max() <= 1e-5 * 0.003 * 10 + 1e-6 * np.abs(pw).max()
+
+
+def test_fused_local_sgd_step_matches_stages(oracle):
+    """dmb_step_sgd_local (one pass) == prepare -> merge(R=1) -> apply"""
+    import ctypes as C
+
+    p = P()
+    from paper_2502_06728_b200 import _capi
+    from paper_2502_06728_b200.core import _ptr, _stream, context
+
+    n = 64 * 1000 + 7
+    cfg = p.ReplicatorConfig(p.Scheme.DeMo, 64, 32, 0.5, True, seed=1234)
+    opt = p.OptimizerConfig(momentum_decay=0.9)
+    g = torch.randn(n, device="cuda") * 1e-3
+    m0 = torch.randn(n, device="cuda") * 1e-3
+    p0 = torch.randn(n, device="cuda") * 0.02
+    st = p.MomentumState(m=m0.clone())
+    enc = p.demo_sgd_prepare(st, g, opt, cfg, 4, 0)
+    q = p.decode_and_merge([enc.update], cfg)
+    p_ref = p0.clone()
+    p.demo_sgd_apply(p_ref, q, 0.01)
+    m_out = torch.empty_like(m0)
+    p_out = torch.empty_like(p0)
+    hdr = _capi.Update()
+    c, o = cfg.c(), opt.c()
+    rc = _capi.lib.dmb_step_sgd_local(context().h, _ptr(g), _ptr(m0), _ptr(m_out), _ptr(p0), _ptr(p_out), n,
+                                      C.byref(o), C.byref(c), 4, 0, 0.01, C.byref(hdr), _stream())
+    assert rc == 0
+    p.status()
+    assert torch.equal(m_out, st.m)
+    assert torch.allclose(p_out, p_ref, rtol=0, atol=1e-7)
+
+
+def test_nonfinite_gradient_refused_before_state_changes():
+    """test_optim.cpp:285-300"""
+    p = P()
+    n = 64 * 4
+    st = p.MomentumState.make(p.OptimizerKind.DemoSgd, n)
+    st.m.fill_(0.5)
+    bad = torch.ones(n, device="cuda")
+    bad[77] = float("nan")
+    with pytest.raises(p.TrainingError, match="77"):
+        p.demo_sgd_prepare(st, bad, p.OptimizerConfig(), p.ReplicatorConfig(p.Scheme.Full, compression=1.0), 0, 0)
+    assert torch.all(st.m == 0.5)
+    bad[77] = float("inf")
+    with pytest.raises(p.TrainingError):
+        p.adamw_prepare(bad, p.ReplicatorConfig(p.Scheme.DeMo, 64, 8), 0, 0)
+    with pytest.raises(p.ProtocolError):
+        p.demo_sgd_prepare(st, torch.ones(n - 1, device="cuda"), p.OptimizerConfig(),
+                           p.ReplicatorConfig(p.Scheme.Full, compression=1.0), 0, 0)
+    p.status()  # latch cleared
+
+
+def test_merge_protocol_errors():
+    """test_replicate.cpp:345-367"""
+    p = P()
+    v = torch.randn(64, device="cuda")
+    cfg = p.ReplicatorConfig(p.Scheme.DeMo, 32, 4, sign_mode=False)
+    ok = p.select_and_encode(v, cfg, 4, 2).update
+    with pytest.raises(p.ProtocolError):
+        p.decode_and_merge([], cfg)
+    for kw in (dict(step=5), dict(shard_id=3), dict(empty=1), dict(n_values=ok.value_count() - 1)):
+        with pytest.raises(p.ProtocolError):
+            p.decode_and_merge([ok, ok.with_header(**kw)], cfg)
+    with pytest.raises(p.ProtocolError):
+        p.decode_and_merge([ok], p.ReplicatorConfig(p.Scheme.Random, compression=0.125))
+
+
+def test_serialize_roundtrip_and_corruption():
+    p = P()
+    v = torch.randn(96, device="cuda")
+    cfg = p.ReplicatorConfig(p.Scheme.DeMo, 32, 5, sign_mode=False)
+    u = p.select_and_encode(v, cfg, 2, 7).update
+    buf = p.serialize(u, cfg.transfer_dtype)
+    assert len(buf) == 9 + u.bytes
+    back = p.deserialize(buf, cfg.transfer_dtype, u)
+    assert torch.equal(back.freq_indices, u.freq_indices) and torch.equal(back.values, u.values)
+    with pytest.raises(p.ProtocolError):
+        p.deserialize(buf[:-3], cfg.transfer_dtype, u)
+    with pytest.raises(p.ProtocolError):
+        p.deserialize(bytes([9]) + buf[1:], cfg.transfer_dtype, u)
+    with pytest.raises(p.ProtocolError):
+        p.deserialize(bytes([2]) + buf[1:], cfg.transfer_dtype, u)
+
+
+def test_grad_mean_member_order(golden):
+    p = P()
+    g = golden["optim"]
+    ins = [dev(x) for x in g["rs_in"]]
+    out = host(p.grad_mean(ins))
+    chunk_close(out, g["rs_out"].reshape(-1), 257, tol=1e-6, what="grad mean")
