@@ -1,0 +1,385 @@
+#!/usr/bin/env python3
+"""FlexDeMo / DeToNATION optimizer-step benchmark (BASELINE.json metric:
+optimizer-step params/sec and HBM roofline %).
+
+Default (N=1): config 4 of BASELINE.json -- OLMo-2-1B-shaped parameters
+(L = 1,484,916,736, flat, synthetic), decoupled AdamW, DeMo s=64 top_k=32, sign on,
+fp32 wire, one replica group of one member (1x1).  One step = one full FlexDeMo
+optimizer step over the whole parameter set: compress (DCT -> TopK -> sign) ->
+gather (identity at R=1) -> decompress (merge -> IDCT) -> AdamW update, fused in one
+pass over HBM (dmb_step_adamw_local).
+
+N>1 (torchrun): 1xN replication layout (the DDP all-gather layout, cluster.cpp:234):
+each rank prepares its payload (dmb_adamw_prepare), payloads are all-gathered over
+NCCL, and every rank merges + applies (dmb_merge_apply_adamw).  Per-GPU work is
+fixed ("weak"), value = N * L / t.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref, the
+reference core compiled unchanged; else the C restatement) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+OLMO1B = 1_484_916_736
+METRIC = "optimizer-step params/sec (DeMo compress+gather+decompress) and HBM roofline %"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--params", type=int, default=OLMO1B)
+    ap.add_argument("--optimizer", default="adamw", choices=["adamw", "sgd"])
+    ap.add_argument("--chunk", type=int, default=64)
+    ap.add_argument("--topk", type=int, default=32)
+    ap.add_argument("--sign", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 22, help="elements per CPU thread")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 9]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ CPU legs
+def cpu_leg(args, n_threads: int, per_thread: int, reps: int = 1):
+    """One bounded sample of the same workload on the host: each thread runs the
+    reference's adamw_prepare + decode_and_merge(R=1) + adamw_apply (or the DeMo-SGD
+    prepare/merge/apply) on its own chunk-aligned slice.  Returns (params/s, kind, sample)."""
+    import numpy as np
+
+    from oracle.oracle import DEMO, Rep, reference, restatement
+
+    ref = reference()
+    orc = ref if ref is not None else restatement()
+    kind = "reference" if ref is not None else "port"
+    s, k = args.chunk, args.topk
+    per_thread = max(s, (per_thread // s) * s)
+    rep = Rep(scheme=DEMO, chunk_size=s, top_k=k, compression=k / s, sign_mode=bool(args.sign), seed=1234)
+    rng = np.random.default_rng(0)
+    slices = []
+    for _ in range(n_threads):
+        g = (rng.standard_normal(per_thread) * 1e-3).astype(np.float32).astype(np.float64)
+        p = (rng.standard_normal(per_thread) * 0.02).astype(np.float32).astype(np.float64)
+        slices.append(dict(g=g, p=p, a=np.zeros(per_thread), b=np.zeros(per_thread), m=np.zeros(per_thread)))
+
+    def work(sl):
+        if args.optimizer == "adamw":
+            e = orc.select_and_encode(sl["g"], rep, 1, 0)
+            q = orc.decode_and_merge(rep, [e["values"]], [e["freq_indices"]], len(sl["g"]), 1, 0)
+            orc.adamw_apply(sl["p"], sl["a"], sl["b"], 0, sl["g"], e["local_q"], q, 0.9, 0.999, 1e-8, 0.0, 1e-3)
+        else:
+            e = orc.demo_sgd_prepare(sl["m"], sl["g"], 0.9, rep, 1, 0)
+            q = orc.decode_and_merge(rep, [e["values"]], [e["freq_indices"]], len(sl["g"]), 1, 0)
+            orc.demo_sgd_apply(sl["p"], q, 0.01)
+
+    times = []
+    for _ in range(reps):
+        th = [threading.Thread(target=work, args=(sl,)) for sl in slices]
+        t0 = time.perf_counter()
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    total = n_threads * per_thread
+    sample = (f"{n_threads} threads x {per_thread} params ({total} total, chunk-aligned slices of the same "
+              f"workload: {'adamw_prepare+decode_and_merge(R=1)+adamw_apply' if args.optimizer == 'adamw' else 'demo_sgd_prepare+decode_and_merge(R=1)+demo_sgd_apply'}, "
+              f"s={s} k={k} sign={'on' if args.sign else 'off'}), median of {reps}, {t:.2f} s")
+    return total / t, kind, sample
+
+
+def config_dict(args, n):
+    return {"workload": "OLMo-2-1B-shaped flat parameters (config 4), decoupled AdamW" if args.optimizer == "adamw"
+            else "OLMo-2-1B-shaped flat parameters, DeMo-SGD",
+            "params": args.params, "scheme": "demo", "chunk_size": args.chunk, "top_k": args.topk,
+            "sign": bool(args.sign), "transfer_dtype": "fp32",
+            "layout": f"1x{n} (shard x replica)", "optimizer": args.optimizer,
+            "l2": "inputs (>= 4 x 5.9 GB) larger than L2 (126 MB)"}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    n_threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_leg(args, n_threads, args.cpu_sample // 4)
+    vals = []
+    t_all = 0.0
+    for _ in range(args.steps):
+        v, kind, sample = cpu_leg(args, n_threads, args.cpu_sample)
+        vals.append(v)
+        t_all += n_threads * args.cpu_sample / v
+    v = statistics.median(vals)
+    line = {"metric": METRIC, "value": v, "unit": "params/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * args.params / v, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "config": config_dict(args, args.gpus),
+            "cpu_baseline": {"value": v, "unit": "params/s", "cores": n_threads, "kind": kind, "sample": sample},
+            "e2e": {"value": v, "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "ms_per_step extrapolates the sampled rate to the full parameter count"}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2502_06728_b200 as P
+    from paper_2502_06728_b200 import _capi
+    from paper_2502_06728_b200.core import context
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    lib = _capi.lib
+    ctx = context(local_rank).h
+    stream = torch.cuda.current_stream(dev)
+    sp = C.c_void_p(stream.cuda_stream)
+    L = args.params
+    cfg = P.ReplicatorConfig(P.Scheme.DeMo, args.chunk, args.topk, args.topk / args.chunk, bool(args.sign),
+                             P.TransferDtype.Fp32, 1234)
+    opt = P.OptimizerConfig(P.OptimizerKind.DecoupledAdamW if args.optimizer == "adamw" else P.OptimizerKind.DemoSgd,
+                            learning_rate=1e-3, momentum_decay=0.9)
+    c, o = cfg.c(), opt.c()
+
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    grad = torch.empty(L, dtype=torch.float32, device=dev).normal_(0.0, 1e-3, generator=gen)
+    params = torch.empty(L, dtype=torch.float32, device=dev).normal_(0.0, 0.02, generator=gen)
+    if args.optimizer == "adamw":
+        s1 = torch.zeros(L, dtype=torch.float32, device=dev)
+        s2 = torch.zeros(L, dtype=torch.float32, device=dev)
+    else:
+        s1 = torch.zeros(L, dtype=torch.float32, device=dev)  # momentum (in place)
+        s2 = None
+    steps = C.c_uint64(0)
+    cap = int(lib.dmb_update_capacity(C.byref(c), L))
+    distributed = world > 1
+    if distributed:
+        import torch.distributed as dist
+
+        own = torch.empty(cap, dtype=torch.uint8, device=dev)
+        gathered = torch.empty(world * cap, dtype=torch.uint8, device=dev)
+        hdr_own = _capi.Update()
+        hdr_own.body = own.data_ptr()
+        ups = (_capi.Update * world)()
+
+    def check(rc):
+        if rc != 0:
+            raise RuntimeError(lib.dmb_last_error().decode())
+
+    def step_once(step):
+        if not distributed:
+            if args.optimizer == "adamw":
+                check(lib.dmb_step_adamw_local(ctx, grad.data_ptr(), params.data_ptr(), params.data_ptr(),
+                                               s1.data_ptr(), s1.data_ptr(), s2.data_ptr(), s2.data_ptr(),
+                                               C.byref(steps), L, C.byref(o), C.byref(c), step, 0, 1e-3, None, sp))
+            else:
+                check(lib.dmb_step_sgd_local(ctx, grad.data_ptr(), s1.data_ptr(), s1.data_ptr(), params.data_ptr(),
+                                             params.data_ptr(), L, C.byref(o), C.byref(c), step, 0, 1e-3, None, sp))
+            return
+        # 1xN: prepare -> NCCL all-gather of fixed-size payloads -> merge + apply
+        if args.optimizer == "adamw":
+            check(lib.dmb_adamw_prepare(ctx, grad.data_ptr(), L, C.byref(c), step, 0, C.byref(hdr_own), None, sp))
+        else:
+            check(lib.dmb_demo_sgd_prepare(ctx, grad.data_ptr(), s1.data_ptr(), s1.data_ptr(), L, C.byref(o),
+                                           C.byref(c), step, 0, C.byref(hdr_own), None, None, sp))
+        dist.all_gather_into_tensor(gathered, own)
+        for r in range(world):
+            ups[r] = hdr_own
+            ups[r].body = gathered.data_ptr() + r * cap
+        if args.optimizer == "adamw":
+            check(lib.dmb_merge_apply_adamw(ctx, ups, world, rank, C.byref(c), params.data_ptr(), s1.data_ptr(),
+                                            s2.data_ptr(), C.byref(steps), grad.data_ptr(), L, step, C.byref(o),
+                                            1e-3, sp))
+        else:
+            check(lib.dmb_merge_apply_sgd(ctx, ups, world, C.byref(c), params.data_ptr(), None, L, step, 1e-3, sp))
+
+    def barrier():
+        if distributed:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for w in range(args.warmup):
+        step_once(w)
+    P.status(dev)
+    barrier()
+
+    # ---- timed region: exactly K steps, CUDA events on the launching stream ----
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = P.launch_count()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    barrier()
+    ev[0].record(stream)
+    for k in range(args.steps):
+        step_once(args.warmup + k)
+        ev[k + 1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = P.launch_count() - launches0
+    P.status(dev)
+    per_step = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    if distributed:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    value = world * L / (ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (the fused step at N=1) ----
+    hbm, peak_kind = peaks()
+    B_alg = 28 if args.optimizer == "adamw" else 20  # bytes per param, SURVEY 8(d)
+    if distributed:
+        # prepare reads g (4); merge+apply reads g again + p/m/v r/w (28) + (1+R) payloads
+        P_b = (args.topk / args.chunk) * 8
+        B_alg = (32 if args.optimizer == "adamw" else 24) + (1 + world) * P_b
+    kern_ms = statistics.median(per_step)
+    achieved = B_alg * L / (kern_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tj = json.load(f)
+        key = f"{args.optimizer}_s{args.chunk}_k{args.topk}_n{world}"
+        traffic = tj.get(key)
+    except Exception:
+        pass
+
+    # ---- e2e: through the C-ABI with host buffers (pinned gradient in, status out) ----
+    e2e = None
+    if not args.no_e2e and not distributed:
+        host_g = torch.empty(L, dtype=torch.float32, pin_memory=True)
+        host_g.copy_(grad)
+        status_h = C.c_int64(-1)
+        ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        e_steps = max(3, min(args.steps, 5))
+        step_once(0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ev2[0].record(stream)
+        for k in range(e_steps):
+            grad.copy_(host_g, non_blocking=True)  # H2D of the step's input
+            step_once(100 + k)
+            check(lib.dmb_status(ctx, sp, C.byref(status_h)))  # D2H of the step result (status word)
+        ev2[1].record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        e_ms = max(ev2[0].elapsed_time(ev2[1]), wall * 1e3) / e_steps
+        e2e = {"value": L / (e_ms * 1e-3), "unit": "params/s", "h2d_bytes_per_step": 4 * L,
+               "d2h_bytes_per_step": 48, "ms_per_step": e_ms,
+               "path": "pinned host gradient -> H2D -> dmb_step_*_local (C-ABI) -> dmb_status D2H"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        n_threads = os.cpu_count() or 1
+        v, kind, sample = cpu_leg(args, n_threads, args.cpu_sample)
+        cpu = {"value": v, "unit": "params/s", "cores": n_threads, "kind": kind, "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "params/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (N(0,1e-3^2) gradients, N(0,0.02^2) params)",
+            "config": config_dict(args, world),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "kernel": "demo_chunk_kernel<StepAdam>" if not distributed else "merge_apply",
+                         "bytes_per_param": B_alg, "peak_source": peak_kind},
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
+            "per_gpu_params_per_s": L / (ms * 1e-3),
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
