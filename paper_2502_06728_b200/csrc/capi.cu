@@ -70,7 +70,17 @@ struct BasisBuf {
   float* B = nullptr;
   float* BT = nullptr;
   double* B64 = nullptr;
+  float* tf32 = nullptr;  // Bhi | Blo | BThi | BTlo, each s*s
 };
+
+// round to TF32 (10 explicit mantissa bits), nearest, ties away: cvt.rna.tf32.f32
+float tf32_rna_host(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
 
 struct RandomKey {
   uint64_t seed = 0, step = 0, len = 0, count = 0;
@@ -92,6 +102,9 @@ struct dmb_ctx {
   RandomScratch rnd{};
   RandomKey rnd_key;
   uint64_t rnd_len_cap = 0;
+  uint32_t* fb_list = nullptr;  // chunks the tensor-core path hands to the FP64 kernel
+  unsigned* fb_count = nullptr;
+  uint64_t fb_cap = 0;
 };
 
 namespace {
@@ -106,7 +119,20 @@ int get_basis(dmb_ctx* ctx, int s, Basis* out) {
         b[(size_t)j * s + i] = (float)b64[(size_t)j * s + i];
         bt[(size_t)i * s + j] = (float)b64[(size_t)j * s + i];
       }
+    std::vector<float> split((size_t)4 * s * s);
+    for (int j = 0; j < s; ++j)
+      for (int i = 0; i < s; ++i) {
+        const double v = b64[(size_t)j * s + i];
+        const float hi = tf32_rna_host((float)v);
+        const float lo = tf32_rna_host((float)(v - (double)hi));
+        split[(size_t)j * s + i] = hi;                      // Bhi[j][i]
+        split[(size_t)s * s + (size_t)j * s + i] = lo;      // Blo[j][i]
+        split[(size_t)2 * s * s + (size_t)i * s + j] = hi;  // BThi[i][j]
+        split[(size_t)3 * s * s + (size_t)i * s + j] = lo;  // BTlo[i][j]
+      }
     BasisBuf buf;
+    DMB_CUDA_TRY(cudaMalloc(&buf.tf32, split.size() * sizeof(float)));
+    DMB_CUDA_TRY(cudaMemcpy(buf.tf32, split.data(), split.size() * sizeof(float), cudaMemcpyHostToDevice));
     DMB_CUDA_TRY(cudaMalloc(&buf.B, b.size() * sizeof(float)));
     DMB_CUDA_TRY(cudaMalloc(&buf.BT, bt.size() * sizeof(float)));
     DMB_CUDA_TRY(cudaMalloc(&buf.B64, b64.size() * sizeof(double)));
@@ -119,6 +145,24 @@ int get_basis(dmb_ctx* ctx, int s, Basis* out) {
   out->B = it->second.B;
   out->BT = it->second.BT;
   out->B64 = it->second.B64;
+  const size_t ss = (size_t)s * s;
+  out->Bhi = it->second.tf32;
+  out->Blo = it->second.tf32 + ss;
+  out->BThi = it->second.tf32 + 2 * ss;
+  out->BTlo = it->second.tf32 + 3 * ss;
+  return DMB_OK;
+}
+
+// fallback-list scratch for the tensor-core path (one slot per chunk)
+int attach_fallback(dmb_ctx* ctx, ChunkArgs* a) {
+  if (a->geo.nchunks > ctx->fb_cap) {
+    cudaFree(ctx->fb_list);
+    DMB_CUDA_TRY(cudaMalloc(&ctx->fb_list, (a->geo.nchunks + 1) * sizeof(uint32_t)));
+    ctx->fb_cap = a->geo.nchunks;
+  }
+  if (!ctx->fb_count) DMB_CUDA_TRY(cudaMalloc(&ctx->fb_count, sizeof(unsigned)));
+  a->fb_list = ctx->fb_list;
+  a->fb_count = ctx->fb_count;
   return DMB_OK;
 }
 
@@ -410,6 +454,7 @@ int encode(dmb_ctx* ctx, DevStatus* st, bool sgd, const float* g, const float* m
     a.body = static_cast<uint8_t*>(out->body);
     a.sgd = sgd_scalars(beta, 0.0);
     a.status = st;
+    if (int rc = attach_fallback(ctx, &a)) return rc;
     launch_chunk_kernel(sgd ? ChunkMode::EncodeSgd : ChunkMode::EncodeAdam, a, s);
     return last_launch();
   }
@@ -448,7 +493,10 @@ int dmb_ctx_create(int device, dmb_ctx** out) {
 int dmb_ctx_destroy(dmb_ctx* ctx) {
   if (!ctx) return DMB_OK;
   cudaSetDevice(ctx->device);
+  cudaFree(ctx->fb_list);
+  cudaFree(ctx->fb_count);
   for (auto& kv : ctx->bases) {
+    cudaFree(kv.second.tf32);
     cudaFree(kv.second.B);
     cudaFree(kv.second.BT);
     cudaFree(kv.second.B64);
@@ -744,6 +792,7 @@ int dmb_step_sgd_local(dmb_ctx* ctx, const float* grad, const float* m_in, float
     a.body = out ? static_cast<uint8_t*>(out->body) : nullptr;
     a.sgd = sgd_scalars(opt->momentum_decay, lr);
     a.status = ctx->status;
+    if (int rc = attach_fallback(ctx, &a)) return rc;
     launch_chunk_kernel(ChunkMode::StepSgd, a, s);
     return last_launch();
   }
@@ -780,6 +829,7 @@ int dmb_step_adamw_local(dmb_ctx* ctx, const float* grad, const float* p_in, flo
   a.body = out ? static_cast<uint8_t*>(out->body) : nullptr;
   a.adam = adam_scalars(opt, *steps, lr);
   a.status = ctx->status;
+  if (int rc = attach_fallback(ctx, &a)) return rc;
   launch_chunk_kernel(ChunkMode::StepAdam, a, s);
   return last_launch();
 }

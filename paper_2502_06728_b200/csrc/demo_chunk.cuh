@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(kThreads) demo_chunk_kernel(const ChunkArgs a)
   if (kMerge || kStep) {
     if (step_failed(a.status)) return;  // state untouched after a TrainingError
   }
+  if (a.list && *a.list_count == 0) return;  // nothing left uncertified
 
   float* sB = smem;
   float* sBT = smem + (smem_basis ? s * s : 0);
@@ -180,8 +181,10 @@ __global__ void __launch_bounds__(kThreads) demo_chunk_kernel(const ChunkArgs a)
   const float eps_scale = (float)((s + 3) * 5.9604644775390625e-08 * sqrt(2.0 / s) * 1.01);
 
   const uint64_t warps_total = (uint64_t)gridDim.x * kWarps;
-  for (uint64_t c0 = ((uint64_t)blockIdx.x * kWarps + warp) * CH; c0 < nchunks;
-       c0 += warps_total * CH) {
+  const bool list_mode = a.list != nullptr;
+  const uint64_t n_units = list_mode ? (uint64_t)*a.list_count : nchunks;
+  for (uint64_t u0 = ((uint64_t)blockIdx.x * kWarps + warp) * CH; u0 < n_units; u0 += warps_total * CH) {
+    const uint64_t c0 = list_mode ? (uint64_t)a.list[u0] : u0;  // list mode: CH == 1
     float x[CH][E];    // encode: v (m_acc or g); merge-adam: g
     float gv[CH][E];   // raw gradient (adam paths)
     float Q[CH][E];    // merged update
@@ -278,6 +281,7 @@ __global__ void __launch_bounds__(kThreads) demo_chunk_kernel(const ChunkArgs a)
         const bool need_signs = sign_mode || dtype == DMB_TERNARY;
         bool uncertain = k < s ? !(kth - nxt > 2.0f * eps) : (need_signs && !(kth > eps));
         if (isnan(l1)) uncertain = false;  // non-finite input: the step fails anyway
+        if (a.force_fp64) uncertain = true;
         double cd[E];
         const bool fp64 = uncertain;
         if (fp64) {
@@ -454,6 +458,7 @@ void launch_t(const ChunkArgs& a, cudaStream_t stream) {
   const uint64_t units = (a.geo.nchunks + (uint64_t)kWarps * CH - 1) / ((uint64_t)kWarps * CH);
   uint64_t grid = (uint64_t)sms * 4;
   if (units < grid) grid = units ? units : 1;
+  if (a.list) grid = (uint64_t)sms;  // list length lives on the device
   kern<<<(unsigned)grid, kThreads, smem, stream>>>(a);
 }
 

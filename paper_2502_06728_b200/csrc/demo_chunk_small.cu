@@ -1,8 +1,30 @@
 // demo_chunk_small.cu -- instantiations for chunk sizes s <= 64 (E = 1, 2; CH = 4)
 // and the mode dispatcher.
+#include <cstdlib>
+
 #include "demo_chunk.cuh"
 
 namespace dmb {
+// DMB_TC=0 forces the SIMT path (A/B checks); read per launch so tests can flip it
+bool tc_enabled() {
+  const char* e = std::getenv("DMB_TC");
+  return !(e && e[0] == '0');
+}
+
+void launch_chunk_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) {
+  if (tc_enabled() && a.fb_list && a.fb_count && tc_supported(mode, a)) {
+    cudaMemsetAsync(a.fb_count, 0, sizeof(unsigned), stream);
+    launch_tc_kernel(mode, a, stream);
+    ChunkArgs fix = a;
+    fix.list = a.fb_list;
+    fix.list_count = a.fb_count;
+    fix.force_fp64 = 1;
+    launch_chunk_simt(mode, fix, stream);
+    return;
+  }
+  launch_chunk_simt(mode, a, stream);
+}
+
 void launch_chunk_large(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream);
 namespace {
 using chunk_impl::launch_t;
@@ -14,7 +36,22 @@ void dispatch_small(const ChunkArgs& a, cudaStream_t stream) {
 }
 }  // namespace
 
-void launch_chunk_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) {
+template <ChunkMode MODE>
+void dispatch_list(const ChunkArgs& a, cudaStream_t stream) {
+  launch_t<2, 1, MODE>(a, stream);
+}
+
+void launch_chunk_simt(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) {
+  if (a.list) {  // FP64 re-derivation of the chunks the tensor-core kernel could not certify
+    switch (mode) {
+      case ChunkMode::EncodeSgd: dispatch_list<ChunkMode::EncodeSgd>(a, stream); break;
+      case ChunkMode::EncodeAdam: dispatch_list<ChunkMode::EncodeAdam>(a, stream); break;
+      case ChunkMode::StepSgd: dispatch_list<ChunkMode::StepSgd>(a, stream); break;
+      case ChunkMode::StepAdam: dispatch_list<ChunkMode::StepAdam>(a, stream); break;
+      default: break;
+    }
+    return;
+  }
   if (a.geo.s > 64) {
     launch_chunk_large(mode, a, stream);
     return;

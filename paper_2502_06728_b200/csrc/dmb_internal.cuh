@@ -116,6 +116,11 @@ struct Basis {
   const float* B;    // [j][i] row-major, s*s
   const float* BT;   // [i][j] transposed
   const double* B64; // [j][i] row-major
+  // TF32 splits for the tensor-core path (hi = RNA_tf32(B64), lo = RNA_tf32(B64 - hi))
+  const float* Bhi;
+  const float* Blo;
+  const float* BThi;
+  const float* BTlo;
 };
 
 enum class ChunkMode : int {
@@ -148,9 +153,21 @@ struct ChunkArgs {
   SgdScalars sgd;
   AdamScalars adam;
   DevStatus* status;
+  // tensor-core path: chunks whose FP32 TopK is not certified go to this list and are
+  // re-derived in FP64 by the SIMT kernel in list mode (list / list_count, force_fp64)
+  uint32_t* fb_list;
+  unsigned* fb_count;
+  const uint32_t* list;
+  const unsigned* list_count;
+  int force_fp64;
 };
 
+// Dispatch: tensor-core kernel + FP64 fix-up for s == 64 when enabled, else SIMT.
 void launch_chunk_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream);
+void launch_chunk_simt(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream);
+bool tc_supported(ChunkMode mode, const ChunkArgs& a);
+void launch_tc_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream);
+bool tc_enabled();
 
 // Elementwise (Full / DiLoCo / Striding / Random) paths.
 struct SparseSel {
