@@ -153,8 +153,11 @@ int get_basis(dmb_ctx* ctx, int s, Basis* out) {
   return DMB_OK;
 }
 
+unsigned long long* g_dbg = nullptr;  // event timestamps of the next tc3 launch (tuning)
+
 // fallback-list scratch for the tensor-core path (one slot per chunk)
 int attach_fallback(dmb_ctx* ctx, ChunkArgs* a) {
+  a->dbg = g_dbg;
   if (a->geo.nchunks > ctx->fb_cap) {
     cudaFree(ctx->fb_list);
     DMB_CUDA_TRY(cudaMalloc(&ctx->fb_list, (a->geo.nchunks + 1) * sizeof(uint32_t)));
@@ -756,6 +759,7 @@ int dmb_merge_apply_adamw(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_up
     a.es_out = exp_avg_sq;
     a.adam = A;
     a.status = ctx->status;
+    if (int rc = attach_fallback(ctx, &a)) return rc;
     launch_chunk_kernel(ChunkMode::MergeAdam, a, s);
     return last_launch();
   }
@@ -876,6 +880,9 @@ int dmb_fallback_chunks(dmb_ctx* ctx, void* stream, uint64_t* count) {
   *count = a.fallback_chunks + b.fallback_chunks;
   return DMB_OK;
 }
+
+// tuning hook (not in the public header): device buffer of 32 x 16 u64 timestamps
+void dmb_debug_events(unsigned long long* d_buf) { g_dbg = d_buf; }
 
 uint64_t dmb_launch_count(dmb_ctx* ctx) {
   (void)ctx;

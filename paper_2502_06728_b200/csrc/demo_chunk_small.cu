@@ -12,9 +12,11 @@ bool tc_enabled() {
 }
 
 void launch_chunk_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) {
-  if (tc_enabled() && a.fb_list && a.fb_count && tc_supported(mode, a)) {
+  const bool tc3 = tc_enabled() && a.fb_list && a.fb_count && tc3_supported(mode, a);
+  if (tc3 || (tc_enabled() && a.fb_list && a.fb_count && tc_supported(mode, a))) {
     cudaMemsetAsync(a.fb_count, 0, sizeof(unsigned), stream);
-    launch_tc_kernel(mode, a, stream);
+    if (tc3) launch_tc3_kernel(mode, a, stream);
+    else launch_tc_kernel(mode, a, stream);
     ChunkArgs fix = a;
     fix.list = a.fb_list;
     fix.list_count = a.fb_count;
@@ -48,7 +50,8 @@ void launch_chunk_simt(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) 
       case ChunkMode::EncodeAdam: dispatch_list<ChunkMode::EncodeAdam>(a, stream); break;
       case ChunkMode::StepSgd: dispatch_list<ChunkMode::StepSgd>(a, stream); break;
       case ChunkMode::StepAdam: dispatch_list<ChunkMode::StepAdam>(a, stream); break;
-      default: break;
+      case ChunkMode::MergeSgd: dispatch_list<ChunkMode::MergeSgd>(a, stream); break;
+      case ChunkMode::MergeAdam: dispatch_list<ChunkMode::MergeAdam>(a, stream); break;
     }
     return;
   }

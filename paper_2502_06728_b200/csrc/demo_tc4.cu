@@ -1,0 +1,652 @@
+// demo_tc4.cu -- tensor-core DeMo kernel for the AdamW paths at chunk size 64 (the
+// bench headline: OLMo-1B-shaped FlexDeMo + decoupled AdamW on one B200).
+//
+// One persistent CTA per SM, 16 warps, tiles of 128 chunks (8192 parameters).  Per tile:
+//   P0  the p / exp_avg / exp_avg_sq loads of this tile are issued into registers
+//       (coalesced 128-bit), so their HBM latency hides under P1-P6; the gradient tile
+//       of the NEXT tile is already in flight through TMA (2-stage ring, 128B swizzle);
+//   P1  split X into TF32 hi / lo (4 threads per chunk, 16 values each) -> smem A;
+//   P2  forward DCT  C = X B^T  as 3xTF32 tcgen05.mma (M=128, N=64, K=64) -> TMEM;
+//   P3  TMEM -> smem transpose (tcgen05.ld 32x32b: warp w reads lane quadrant w%4,
+//       columns 16 (w/4) ... +16);
+//   P4  per chunk (a quad of lanes): TopK by MSB radix select with quad reductions,
+//       certification against the FP64 oracle, exact FP64 re-derivation of the
+//       coefficients the FP32 bound cannot order (oracle operation order), payload,
+//       W = wire - coef on the selection (= Q - local_q of a one-member group) -> smem A;
+//   P5  inverse DCT  D = W B  (3xTF32) -> TMEM;   P6  TMEM -> smem;
+//   P7  AdamW update g' = g + D with the prefetched state, 128-bit coalesced stores.
+// Modes: StepAdam (prepare + merge(R=1) + apply, optim.cpp:51-74 / replicate.cpp:282-309),
+// MergeAdam (R gathered payloads + own indices), EncodeAdam (payload only).  The one
+// partial chunk at the shard end goes to the SIMT kernel through the fallback list.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cfloat>
+#include <mutex>
+
+#include "dmb_internal.cuh"
+#include "tc_ptx.cuh"
+
+namespace dmb {
+namespace {
+
+using namespace ptx;
+
+constexpr int S = 64;
+constexpr int TM = 128;
+constexpr int NG = 2;
+constexpr int THREADS = 512;
+constexpr int WARPS = THREADS / 32;
+
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(S >> 3) << 17) |
+                           ((uint32_t)(TM >> 4) << 24);
+
+constexpr uint32_t TILE = TM * S * 4;   // 32 KB
+constexpr uint32_t BMAT = S * 128 * 2;  // 16 KB
+constexpr uint32_t OFF_BHI = 0;         // B[j][i]   forward operand (K-major SW128)
+constexpr uint32_t OFF_BLO = BMAT;
+constexpr uint32_t OFF_BTHI = 2 * BMAT;  // B^T[i][j] inverse operand
+constexpr uint32_t OFF_BTLO = 3 * BMAT;
+constexpr uint32_t OFF_AHI = 4 * BMAT;   // A operand hi (X, then W); scratch in P4
+constexpr uint32_t OFF_ALO = OFF_AHI + TILE;
+constexpr uint32_t OFF_G = OFF_ALO + TILE;  // NG gradient tiles (TMA, swizzled)
+constexpr uint32_t OFF_C = OFF_G + NG * TILE;  // coefficient tile, then the D tile
+constexpr uint32_t OFF_L1 = OFF_C + TILE;      // per-row ||x||_1 (128 floats)
+constexpr uint32_t OFF_BAR = OFF_L1 + 512;
+constexpr uint32_t SMEM_BYTES = OFF_BAR + 64;
+static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+constexpr uint32_t TMEM_COLS = 128;  // D1 at 0, D2 at 64
+
+constexpr float kEpsScale = 1.52587890625e-05f * 0.1767766952966369f * 1.01f;  // 2^-16 sqrt(2/64)
+
+__device__ __forceinline__ uint32_t sw_off(int r, int q) {
+  return (uint32_t)(q >> 3) * (TM * 128u) + (uint32_t)r * 128u + ((uint32_t)((q & 7) ^ (r & 7)) << 4);
+}
+__device__ __forceinline__ uint32_t sw_off_b(int r, int q) {
+  return (uint32_t)(q >> 3) * (S * 128u) + (uint32_t)r * 128u + ((uint32_t)((q & 7) ^ (r & 7)) << 4);
+}
+
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ int quad_sum(int v) {
+  v += __shfl_xor_sync(kFull, v, 1);
+  v += __shfl_xor_sync(kFull, v, 2);
+  return v;
+}
+__device__ __forceinline__ float quad_sumf(float v) {
+  v += __shfl_xor_sync(kFull, v, 1);
+  v += __shfl_xor_sync(kFull, v, 2);
+  return v;
+}
+__device__ __forceinline__ float quad_min(float v) {
+  v = fminf(v, __shfl_xor_sync(kFull, v, 1));
+  return fminf(v, __shfl_xor_sync(kFull, v, 2));
+}
+__device__ __forceinline__ float quad_max(float v) {
+  v = fmaxf(v, __shfl_xor_sync(kFull, v, 1));
+  return fmaxf(v, __shfl_xor_sync(kFull, v, 2));
+}
+// exclusive prefix within the quad (lanes ordered by slice)
+__device__ __forceinline__ int quad_excl(int v, int slice) {
+  int s = v;
+  const int a = __shfl_up_sync(kFull, s, 1);
+  if (slice >= 1) s += a;
+  const int b = __shfl_up_sync(kFull, s, 2);
+  if (slice >= 2) s += b;
+  return s - v;
+}
+
+__device__ __forceinline__ int count_ge16(const float (&c)[16], float t) {
+  int n0 = 0, n1 = 0, n2 = 0, n3 = 0;
+#pragma unroll
+  for (int j = 0; j < 16; j += 4) {
+    n0 += fabsf(c[j]) >= t;
+    n1 += fabsf(c[j + 1]) >= t;
+    n2 += fabsf(c[j + 2]) >= t;
+    n3 += fabsf(c[j + 3]) >= t;
+  }
+  return (n0 + n1) + (n2 + n3);
+}
+
+// TopK of a 64-coefficient row spread over a quad (16 per lane, lane = slice): MSB radix
+// select on |c| (float compares on non-negative values order like their bit patterns),
+// early exit once exactly k clear the threshold, ties toward the lower index.  All 32
+// lanes iterate together (rows that are done just stop updating).
+__device__ __forceinline__ uint32_t topk_quad(const float (&c)[16], int k, int slice, bool active) {
+  uint32_t T = 0;
+  bool done = !active, exact = false;
+#pragma unroll 1
+  for (int b = 30; b >= 0; --b) {
+    if (__all_sync(kFull, done)) break;
+    const uint32_t cand = T | (1u << b);
+    const int cnt = quad_sum(count_ge16(c, __uint_as_float(cand)));
+    if (!done && cnt >= k) {
+      T = cand;
+      if (cnt == k) {
+        exact = true;
+        done = true;
+      }
+    }
+  }
+  const float Tf = __uint_as_float(T);
+  uint32_t sel = 0;
+  int gt = 0, eq = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float m = fabsf(c[j]);
+    gt += m > Tf;
+    eq += m == Tf;
+  }
+  const int gt_all = quad_sum(gt);
+  const int eq_before = quad_excl(eq, slice);
+  int need = k - gt_all - eq_before;  // ties this lane may still take (index order = slice order)
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float m = fabsf(c[j]);
+    bool take = m > Tf;
+    if (exact) take = m >= Tf;
+    else if (m == Tf) {
+      take = need > 0;
+      --need;
+    }
+    if (take) sel |= 1u << j;
+  }
+  return active ? sel : 0u;
+}
+
+template <ChunkMode MODE>
+__global__ void __launch_bounds__(THREADS, 1) demo_tc4_kernel(const ChunkArgs a, const __grid_constant__ CUtensorMap gmap) {
+  constexpr bool kEncodeOnly = MODE == ChunkMode::EncodeAdam;
+  constexpr bool kMerge = MODE == ChunkMode::MergeAdam;
+
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023u) != 0u) __trap();
+  uint64_t* g_full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* mma_bar = g_full + NG;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_bar + 1);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+  // quad mapping: chunk row 8w + lane/4, slice lane%4 (columns 16 slice .. +15)
+  const int qrow = 8 * warp + (lane >> 2);
+  const int slice = lane & 3;
+  // TMEM mapping: lane quadrant w%4 (rows 32 (w%4) + lane), columns 16 (w/4) .. +15
+  const int trow = 32 * (warp & 3) + lane;
+  const int tcol = 16 * (warp >> 2);
+  const uint32_t tlane = (uint32_t)(32 * (warp & 3)) << 16;
+
+  if (!kEncodeOnly && step_failed(a.status)) return;
+
+  for (int u = tid; u < S * 16; u += THREADS) {
+    const int r = u >> 4, q = u & 15;
+    *reinterpret_cast<float4*>(smem + OFF_BHI + sw_off_b(r, q)) = *reinterpret_cast<const float4*>(a.basis.Bhi + r * S + 4 * q);
+    *reinterpret_cast<float4*>(smem + OFF_BLO + sw_off_b(r, q)) = *reinterpret_cast<const float4*>(a.basis.Blo + r * S + 4 * q);
+    *reinterpret_cast<float4*>(smem + OFF_BTHI + sw_off_b(r, q)) = *reinterpret_cast<const float4*>(a.basis.BThi + r * S + 4 * q);
+    *reinterpret_cast<float4*>(smem + OFF_BTLO + sw_off_b(r, q)) = *reinterpret_cast<const float4*>(a.basis.BTlo + r * S + 4 * q);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < NG; ++s) mbar_init(&g_full[s], 1);
+    mbar_init(mma_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, TMEM_COLS);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const uint64_t len = a.geo.len;
+  const uint64_t nchunks = a.geo.nchunks;
+  const uint64_t ntiles = (nchunks + TM - 1) / TM;
+  const int k = a.geo.k;
+  const int dtype = a.geo.dtype;
+  const bool sign_mode = a.geo.sign_mode;
+  const bool need_signs = sign_mode || dtype == DMB_TERNARY;
+  const bool full_band = k == S;
+  const uint64_t nvals = nchunks * (uint64_t)k;
+  const bool partial_last = (len % S) != 0;
+  const uint32_t s_base = smem_u32(smem);
+  uint8_t* a_hi = smem + OFF_AHI;
+  uint8_t* a_lo = smem + OFF_ALO;
+  uint8_t* ct = smem + OFF_C;
+  uint32_t mma_phase = 0;
+  const AdamScalars A = a.adam;
+
+  auto issue = [&](uint32_t d, uint32_t bh, uint32_t bl) {  // D = Ahi Bh + Ahi Bl + Alo Bh
+    const uint32_t ahi = s_base + OFF_AHI, alo = s_base + OFF_ALO;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const uint32_t ao = (uint32_t)(kk >> 2) * (TM * 128u) + (uint32_t)(kk & 3) * 32u;
+      const uint32_t bo = (uint32_t)(kk >> 2) * (S * 128u) + (uint32_t)(kk & 3) * 32u;
+      mma_tf32(d, desc_sw128(ahi + ao), desc_sw128(bh + bo), IDESC, kk > 0 ? 1u : 0u);
+      mma_tf32(d, desc_sw128(ahi + ao), desc_sw128(bl + bo), IDESC, 1u);
+      mma_tf32(d, desc_sw128(alo + ao), desc_sw128(bh + bo), IDESC, 1u);
+    }
+    mma_commit(mma_bar);
+  };
+  auto mma_wait = [&]() {
+    mbar_wait(mma_bar, mma_phase);
+    mma_phase ^= 1u;
+    tc_fence_after();
+  };
+  // TMEM columns [col, col+16) of this warp's lane quadrant -> smem tile rows (swizzled)
+  auto tmem_to_tile = [&](uint32_t col) {
+    float v[16];
+    tmem_ld16(tmem + tlane + col + tcol, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      *reinterpret_cast<float4*>(ct + sw_off(trow, (tcol >> 2) + e)) =
+          make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+  };
+
+  if (tid == 0 && blockIdx.x < ntiles) {
+    mbar_arrive_expect_tx(&g_full[0], TILE);
+    tma_2d(smem + OFF_G, &gmap, 0, (int)(blockIdx.x * TM), &g_full[0]);
+    tma_2d(smem + OFF_G + TILE / 2, &gmap, 32, (int)(blockIdx.x * TM), &g_full[0]);
+  }
+
+  uint32_t it = 0;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it % NG;
+    const uint64_t tbase = tile * (uint64_t)TM * S;
+    // next tile's gradient into the other stage (its previous tile is fully consumed)
+    if (tid == 0 && tile + gridDim.x < ntiles) {
+      const int sn = (it + 1) % NG;
+      mbar_arrive_expect_tx(&g_full[sn], TILE);
+      tma_2d(smem + OFF_G + sn * TILE, &gmap, 0, (int)((tile + gridDim.x) * TM), &g_full[sn]);
+      tma_2d(smem + OFF_G + sn * TILE + TILE / 2, &gmap, 32, (int)((tile + gridDim.x) * TM), &g_full[sn]);
+    }
+
+    // ---- P0: prefetch this tile's optimizer state (coalesced, in flight during P1-P6) ----
+    float4 pv[4], ev[4], sv[4];
+    bool live[4];
+    if (!kEncodeOnly) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int u = tid + THREADS * j;
+        const uint64_t row = tile * TM + (u >> 4);
+        live[j] = row < nchunks && !(partial_last && row == nchunks - 1);
+        if (live[j]) {
+          const uint64_t e0 = tbase + 4ull * u;
+          pv[j] = __ldcs(reinterpret_cast<const float4*>(a.p_in + e0));
+          ev[j] = __ldcs(reinterpret_cast<const float4*>(a.ea_in + e0));
+          sv[j] = __ldcs(reinterpret_cast<const float4*>(a.es_in + e0));
+        }
+      }
+    }
+
+    // ---- P1: split the gradient rows into TF32 hi / lo ----
+    const uint64_t row = tile * TM + qrow;
+    const bool row_ok = row < nchunks;
+    const bool tail_row = row_ok && partial_last && row == nchunks - 1;
+    mbar_wait(&g_full[st], (it / NG) & 1);
+    const uint8_t* gs = smem + OFF_G + st * TILE;
+    float l1 = 0.f;
+    {
+      bool finite = true;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int q = 4 * slice + e;
+        float4 v = *reinterpret_cast<const float4*>(gs + sw_off(qrow, q));
+        if (tail_row) {  // partial last chunk, zero padded (transform.cpp:27-32)
+          float* vp = &v.x;
+          for (int z = 0; z < 4; ++z) {
+            const uint64_t gi = row * S + 4 * q + z;
+            vp[z] = gi < len ? a.g[gi] : 0.0f;
+          }
+        }
+        const float xv[4] = {v.x, v.y, v.z, v.w};
+        float h[4], lo[4];
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          l1 += fabsf(xv[z]);
+          finite = finite && isfinite(xv[z]);
+          h[z] = tf32_rna(xv[z]);
+          lo[z] = tf32_rna(xv[z] - h[z]);
+        }
+        *reinterpret_cast<float4*>(a_hi + sw_off(qrow, q)) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(a_lo + sw_off(qrow, q)) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+      }
+      if (!finite) {  // first offending index of this slice (require_finite, vec.cpp:7-16)
+        for (int j = 0; j < 16; ++j) {
+          const int col = 16 * slice + j;
+          float v = *reinterpret_cast<const float*>(gs + sw_off(qrow, col >> 2) + 4 * (col & 3));
+          if (tail_row) v = row * S + col < len ? a.g[row * S + col] : 0.0f;
+          if (!isfinite(v)) {
+            latch_bad(a.status, row * S + col);
+            break;
+          }
+        }
+      }
+      l1 = quad_sumf(l1);
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+
+    // ---- P2: forward DCT ----
+    if (tid == 0) {
+      tc_fence_after();
+      issue(tmem + 0, s_base + OFF_BHI, s_base + OFF_BLO);
+    }
+    mma_wait();
+    // ---- P3: coefficients TMEM -> smem ----
+    tmem_to_tile(0);
+    tc_fence_before();
+    __syncthreads();
+
+    // ---- P4: selection, certification, exact resolution, payload, W ----
+    float c[16];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float4 v = *reinterpret_cast<const float4*>(ct + sw_off(qrow, 4 * slice + e));
+      c[4 * e] = v.x;
+      c[4 * e + 1] = v.y;
+      c[4 * e + 2] = v.z;
+      c[4 * e + 3] = v.w;
+    }
+    __syncthreads();  // every coefficient row is in registers: the C tile may be scratch now
+    const bool active = row_ok && !tail_row;
+    if (tail_row && slice == 0) {
+      const unsigned slot = atomicAdd(a.fb_count, 1u);
+      a.fb_list[slot] = (uint32_t)row;
+    }
+    uint32_t sel = 0;  // this lane's 16 frequencies
+    float grid_w[16];  // merge: grid / R on this lane's frequencies
+    if (!kMerge) {
+      sel = full_band ? (active ? 0xffffu : 0u) : topk_quad(c, k, slice, active);
+      // certification: selection (and signs, when signs travel) provably equal the oracle's
+      float kth = FLT_MAX, nxt = 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float m = fabsf(c[j]);
+        if ((sel >> j) & 1u) kth = fminf(kth, m);
+        else nxt = fmaxf(nxt, m);
+      }
+      kth = quad_min(kth);
+      nxt = quad_max(nxt);
+      const float eps = kEpsScale * l1;
+      bool need_res = false;
+      uint32_t amb = 0, cin = 0;
+      if (active) {
+        const bool sel_unc = !full_band && !(kth - nxt > 2.0f * eps);
+        const bool sign_unc = need_signs && !(kth > eps);
+        need_res = !isnan(l1) && (sel_unc || sign_unc || a.force_fp64);
+        if (need_res) {
+          const float hi_b = a.force_fp64 ? FLT_MAX : nxt + 2.0f * eps;
+          const float lo_b = a.force_fp64 ? 0.0f : kth - 2.0f * eps;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float m = fabsf(c[j]);
+            const bool is_amb = full_band ? (m <= eps || a.force_fp64) : (m >= lo_b && m <= hi_b);
+            if (is_amb) amb |= 1u << j;
+            else if (!full_band && m > hi_b) cin |= 1u << j;
+          }
+        }
+      }
+      // Exact resolution (rare): the whole warp forms the 64 products of one ambiguous
+      // coefficient, lane 0 of the quad sums them sequentially from 0.0 in FP64 in the
+      // oracle's order (transform.cpp:56-63); the selection among the ambiguous set uses
+      // those values (ties -> lower index).  Scratch: the free A rows of the chunk.
+      unsigned todo = __ballot_sync(kFull, need_res && slice == 0);
+      if (todo) {
+        double* prod = reinterpret_cast<double*>(ct) + warp * 64;  // C tile rows are consumed
+        __syncwarp();
+        while (todo) {
+          const int L = __ffs(todo) - 1;  // quad leader lane
+          todo &= todo - 1;
+          const int qr = 8 * warp + (L >> 2);
+          const uint64_t rowL = tile * TM + qr;
+          double* ex = reinterpret_cast<double*>(a_hi) + qr * 32;   // exact values, slots 0..31
+          double* ex2 = reinterpret_cast<double*>(a_lo) + qr * 32;  // slots 32..63
+          // the row's ambiguous mask (64 bit) from the 4 lanes of its quad
+          uint64_t m64 = 0;
+#pragma unroll
+          for (int sl = 0; sl < 4; ++sl) m64 |= (uint64_t)__shfl_sync(kFull, amb, L + sl) << (16 * sl);
+          const float x0 = *reinterpret_cast<const float*>(gs + sw_off(qr, lane >> 2) + 4 * (lane & 3));
+          const float x1 = *reinterpret_cast<const float*>(gs + sw_off(qr, (lane + 32) >> 2) + 4 * (lane & 3));
+          int pos = 0;
+          for (uint64_t m = m64; m; m &= m - 1, ++pos) {
+            const int j = __ffsll((long long)m) - 1;
+            prod[lane] = __dmul_rn(__ldg(a.basis.B64 + j * S + lane), (double)x0);
+            prod[lane + 32] = __dmul_rn(__ldg(a.basis.B64 + j * S + lane + 32), (double)x1);
+            __syncwarp();
+            if (lane == L) {
+              double acc = 0.0;
+#pragma unroll 16
+              for (int ii = 0; ii < 64; ++ii) acc = __dadd_rn(acc, prod[ii]);
+              (pos < 32 ? ex[pos] : ex2[pos - 32]) = acc;
+            }
+            __syncwarp();
+          }
+          // the leader picks the selection among the ambiguous set
+          uint64_t cin64 = 0;
+#pragma unroll
+          for (int sl = 0; sl < 4; ++sl) cin64 |= (uint64_t)__shfl_sync(kFull, cin, L + sl) << (16 * sl);
+          uint64_t chosen = 0;
+          if (lane == L && !full_band) {
+            int need = k - __popcll(cin64);
+            for (; need > 0; --need) {
+              int bj = -1, p = 0;
+              double bv = -1.0;
+              for (uint64_t m = m64; m; m &= m - 1, ++p) {
+                const int j = __ffsll((long long)m) - 1;
+                if ((chosen >> j) & 1ull) continue;
+                const double v = fabs(p < 32 ? ex[p] : ex2[p - 32]);
+                if (v > bv) {
+                  bv = v;
+                  bj = j;
+                }
+              }
+              if (bj < 0) break;
+              chosen |= 1ull << bj;
+            }
+          }
+          chosen = ((uint64_t)__shfl_sync(kFull, (uint32_t)(chosen >> 32), L) << 32) |
+                   (uint64_t)__shfl_sync(kFull, (uint32_t)chosen, L);
+          __syncwarp();
+          if ((lane >> 2) == (L >> 2)) {  // the quad of this row takes the exact values
+            if (!full_band) sel = (uint32_t)(((cin64 | chosen) >> (16 * slice)) & 0xffffu);
+            const uint32_t mine = amb;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if ((mine >> j) & 1u) {
+                const int gj = 16 * slice + j;
+                const int p = __popcll(m64 & ((1ull << gj) - 1ull));
+                c[j] = (float)(p < 32 ? ex[p] : ex2[p - 32]);
+              }
+            }
+          }
+          __syncwarp();
+        }
+      }
+      // payload: ascending frequency order = slice order, then j
+      const int before = quad_excl(active ? __popc(sel) : 0, slice);
+      if (a.body && active) {
+        uint32_t* idx_out = reinterpret_cast<uint32_t*>(a.body) + row * (uint64_t)k + before;
+        uint8_t* val_out = a.body + nvals * 4;
+        uint64_t tpos = row * (uint64_t)k + before;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if ((sel >> j) & 1u) {
+            *idx_out++ = (uint32_t)(16 * slice + j);
+            store_wire_value(val_out, tpos++, condition_f32(c[j], dtype, sign_mode), dtype);
+          }
+        }
+      }
+    } else {
+      // merged grid of the R gathered payloads (rank order, replicate.cpp:282-300) and
+      // this rank's own selection; the grid lives in the free A rows of the chunk
+      float* grid = reinterpret_cast<float*>(a_hi) + qrow * S;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) grid[16 * slice + j] = 0.0f;
+      __syncwarp();
+      if (row_ok && slice == 0) {
+        for (int rr = 0; rr < a.in.R; ++rr) {
+          const uint32_t* idx_r = reinterpret_cast<const uint32_t*>(a.in.body[rr]) + row * (uint64_t)k;
+          const uint8_t* val_r = a.in.body[rr] + nvals * 4;
+          for (int t = 0; t < k; ++t) {
+            const uint32_t j = idx_r[t];
+            if (j < (uint32_t)S) grid[j] += load_wire_value(val_r, row * (uint64_t)k + t, dtype);
+            else atomicExch(&a.status->protocol_error, 1u);
+          }
+        }
+      }
+      __syncwarp();
+      uint64_t own = 0;
+      if (row_ok && slice == 0) {
+        const uint32_t* idx_o = reinterpret_cast<const uint32_t*>(a.in.body[a.own_rank]) + row * (uint64_t)k;
+        for (int t = 0; t < k; ++t) own |= 1ull << (idx_o[t] & 63u);
+      }
+      own = ((uint64_t)__shfl_sync(kFull, (uint32_t)(own >> 32), lane & ~3) << 32) |
+            (uint64_t)__shfl_sync(kFull, (uint32_t)own, lane & ~3);
+      sel = (uint32_t)((own >> (16 * slice)) & 0xffffu);
+      const float invR = 1.0f / (float)a.in.R;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) grid_w[j] = grid[16 * slice + j] * invR;
+      __syncwarp();
+    }
+
+    __syncthreads();  // A rows held exact-value / grid scratch; W overwrites them next
+    if (kEncodeOnly) continue;
+    // W (this lane's 16 frequencies) -> A as TF32 hi / lo
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float h[4], lo[4];
+#pragma unroll
+      for (int z = 0; z < 4; ++z) {
+        const int j = 4 * e + z;
+        const bool on = (sel >> j) & 1u;
+        float w;
+        if (kMerge) w = grid_w[j] - ((on && !full_band) ? c[j] : 0.0f);
+        else w = full_band ? condition_f32(c[j], dtype, sign_mode)
+                           : (on ? condition_f32(c[j], dtype, sign_mode) - c[j] : 0.0f);
+        if (!active) w = 0.0f;
+        h[z] = tf32_rna(w);
+        lo[z] = tf32_rna(w - h[z]);
+      }
+      *reinterpret_cast<float4*>(a_hi + sw_off(qrow, 4 * slice + e)) = make_float4(h[0], h[1], h[2], h[3]);
+      *reinterpret_cast<float4*>(a_lo + sw_off(qrow, 4 * slice + e)) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+
+    // ---- P5: inverse DCT, P6: D -> smem ----
+    if (tid == 0) {
+      tc_fence_after();
+      issue(tmem + 64, s_base + OFF_BTHI, s_base + OFF_BTLO);
+    }
+    mma_wait();
+    tmem_to_tile(64);
+    tc_fence_before();
+    __syncthreads();
+
+    // ---- P7: AdamW, coalesced (g' = g - local_q + Q = g + D; full band: D) ----
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (!live[j]) continue;
+      const int u = tid + THREADS * j;
+      const int rr = u >> 4, q = u & 15;
+      const uint64_t e0 = tbase + 4ull * u;
+      const float4 g4 = *reinterpret_cast<const float4*>(gs + sw_off(rr, q));
+      const float4 d4 = *reinterpret_cast<const float4*>(ct + sw_off(rr, q));
+      const float gg[4] = {g4.x, g4.y, g4.z, g4.w};
+      const float dd[4] = {d4.x, d4.y, d4.z, d4.w};
+      float* pp = &pv[j].x;
+      float* ep = &ev[j].x;
+      float* sp = &sv[j].x;
+#pragma unroll
+      for (int z = 0; z < 4; ++z) {
+        const float gp = full_band ? dd[z] : gg[z] + dd[z];
+        const float m1 = A.beta1 * ep[z] + A.one_minus_beta1 * gp;
+        const float m2 = A.beta2 * sp[z] + A.one_minus_beta2 * gp * gp;
+        float pn = pp[z] - A.lr * ((m1 * A.inv_bc1) / (sqrtf(m2 * A.inv_bc2) + A.eps));
+        if (A.lr_wd != 0.0f) pn -= A.lr_wd * pn;
+        ep[z] = m1;
+        sp[z] = m2;
+        pp[z] = pn;
+      }
+      __stcs(reinterpret_cast<float4*>(a.p_out + e0), pv[j]);
+      __stcs(reinterpret_cast<float4*>(a.ea_out + e0), ev[j]);
+      __stcs(reinterpret_cast<float4*>(a.es_out + e0), sv[j]);
+    }
+    __syncthreads();  // gradient stage and C tile free for the next tile
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tmem, TMEM_COLS);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+template <ChunkMode MODE>
+void launch_mode(const ChunkArgs& a, const CUtensorMap& map, cudaStream_t stream) {
+  auto kern = demo_tc4_kernel<MODE>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t ntiles = (a.geo.nchunks + TM - 1) / TM;
+  const unsigned grid = (unsigned)(ntiles < (uint64_t)sms ? (ntiles ? ntiles : 1) : sms);
+  kern<<<grid, THREADS, SMEM_BYTES, stream>>>(a, map);
+}
+
+}  // namespace
+
+bool tc3_supported(ChunkMode mode, const ChunkArgs& a) {
+  if (a.geo.s != S || a.basis.Bhi == nullptr || encode_fn() == nullptr) return false;
+  if (!(mode == ChunkMode::StepAdam || mode == ChunkMode::MergeAdam || mode == ChunkMode::EncodeAdam))
+    return false;
+  if (a.local_q || a.m_accum || a.q_out) return false;  // inspection outputs: generic kernels
+  if (a.geo.len / S == 0) return false;                 // the tensor map needs one whole chunk
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  return al(a.g) && al(a.p_in) && al(a.p_out) && al(a.ea_in) && al(a.ea_out) && al(a.es_in) && al(a.es_out);
+}
+
+void launch_tc3_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) {
+  count_launches(1);
+  // gradient as [whole chunks x 64] fp32, boxes of 128 rows x 32 columns, 128B swizzle;
+  // rows past the end read as zeros (the partial last chunk goes to the SIMT kernel)
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)S, (cuuint64_t)(a.geo.len / S)};
+  const cuuint64_t strides[1] = {(cuuint64_t)S * 4};
+  const cuuint32_t box[2] = {32, TM};
+  const cuuint32_t estr[2] = {1, 1};
+  encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.g), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  switch (mode) {
+    case ChunkMode::StepAdam: launch_mode<ChunkMode::StepAdam>(a, map, stream); break;
+    case ChunkMode::MergeAdam: launch_mode<ChunkMode::MergeAdam>(a, map, stream); break;
+    case ChunkMode::EncodeAdam: launch_mode<ChunkMode::EncodeAdam>(a, map, stream); break;
+    default: break;
+  }
+}
+
+}  // namespace dmb

@@ -160,6 +160,7 @@ struct ChunkArgs {
   const uint32_t* list;
   const unsigned* list_count;
   int force_fp64;
+  unsigned long long* dbg;  // optional event timestamps (tests / tuning only)
 };
 
 // Dispatch: tensor-core kernel + FP64 fix-up for s == 64 when enabled, else SIMT.
@@ -168,6 +169,8 @@ void launch_chunk_simt(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream);
 bool tc_supported(ChunkMode mode, const ChunkArgs& a);
 void launch_tc_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream);
 bool tc_enabled();
+bool tc3_supported(ChunkMode mode, const ChunkArgs& a);
+void launch_tc3_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream);
 
 // Elementwise (Full / DiLoCo / Striding / Random) paths.
 struct SparseSel {
