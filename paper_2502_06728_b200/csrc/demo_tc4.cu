@@ -114,15 +114,30 @@ __device__ __forceinline__ int count_ge16(const float (&c)[16], float t) {
   return (n0 + n1) + (n2 + n3);
 }
 
-// TopK of a 64-coefficient row spread over a quad (16 per lane, lane = slice): MSB radix
-// select on |c| (float compares on non-negative values order like their bit patterns),
-// early exit once exactly k clear the threshold, ties toward the lower index.  All 32
-// lanes iterate together (rows that are done just stop updating).
+// TopK of a 64-coefficient row spread over a quad (16 per lane, lane = slice): MSB
+// radix select on |c| (float compares on non-negative values order like their bit
+// patterns) with quad reductions.  The search starts below the common bit prefix of the
+// row's smallest and largest |c| (every key shares it) and exits as soon as exactly k
+// keys clear the threshold; ties go to the lower index.  All 32 lanes iterate together
+// (finished rows stop updating).
 __device__ __forceinline__ uint32_t topk_quad(const float (&c)[16], int k, int slice, bool active) {
-  uint32_t T = 0;
-  bool done = !active, exact = false;
+  float mx = 0.f, mn = FLT_MAX;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    mx = fmaxf(mx, fabsf(c[j]));
+    mn = fminf(mn, fabsf(c[j]));
+  }
+  mx = quad_max(mx);
+  mn = quad_min(mn);
+  const uint32_t diff = __float_as_uint(mx) ^ __float_as_uint(mn);
+  const int top = diff ? 31 - __clz(diff) : -1;  // highest bit where keys can differ
+  uint32_t T = top >= 0 ? (__float_as_uint(mx) & ~((2u << top) - 1u)) : __float_as_uint(mx);
+  bool done = !active || top < 0, exact = false;
+  // warp-uniform trip count: bits above a row's own top are in its common prefix, so
+  // extra iterations there leave it unchanged
+  const int top_w = __reduce_max_sync(kFull, (unsigned)(top + 1)) - 1;
 #pragma unroll 1
-  for (int b = 30; b >= 0; --b) {
+  for (int b = top_w; b >= 0; --b) {
     if (__all_sync(kFull, done)) break;
     const uint32_t cand = T | (1u << b);
     const int cnt = quad_sum(count_ge16(c, __uint_as_float(cand)));
@@ -232,9 +247,10 @@ __global__ void __launch_bounds__(THREADS, 1) demo_tc4_kernel(const ChunkArgs a,
     }
     mma_commit(mma_bar);
   };
-  auto mma_wait = [&]() {
-    mbar_wait(mma_bar, mma_phase);
+  auto mma_wait = [&]() {  // one warp parks on the mbarrier, the rest on the CTA barrier
+    if (warp == 0) mbar_wait(mma_bar, mma_phase);
     mma_phase ^= 1u;
+    __syncthreads();
     tc_fence_after();
   };
   // TMEM columns [col, col+16) of this warp's lane quadrant -> smem tile rows (swizzled)
@@ -288,7 +304,8 @@ __global__ void __launch_bounds__(THREADS, 1) demo_tc4_kernel(const ChunkArgs a,
     const uint64_t row = tile * TM + qrow;
     const bool row_ok = row < nchunks;
     const bool tail_row = row_ok && partial_last && row == nchunks - 1;
-    mbar_wait(&g_full[st], (it / NG) & 1);
+    if (warp == 0) mbar_wait(&g_full[st], (it / NG) & 1);
+    __syncthreads();
     const uint8_t* gs = smem + OFF_G + st * TILE;
     float l1 = 0.f;
     {
@@ -569,7 +586,11 @@ __global__ void __launch_bounds__(THREADS, 1) demo_tc4_kernel(const ChunkArgs a,
         const float gp = full_band ? dd[z] : gg[z] + dd[z];
         const float m1 = A.beta1 * ep[z] + A.one_minus_beta1 * gp;
         const float m2 = A.beta2 * sp[z] + A.one_minus_beta2 * gp * gp;
-        float pn = pp[z] - A.lr * ((m1 * A.inv_bc1) / (sqrtf(m2 * A.inv_bc2) + A.eps));
+        // m_hat / (sqrt(v_hat) + eps) with MUFU sqrt / reciprocal (a few ulp, far inside
+        // the 1e-5 update tolerance of the FP64 reference)
+        const float vh = m2 * A.inv_bc2;
+        const float den = __fsqrt_rn(vh) + A.eps;
+        float pn = pp[z] - A.lr * __fdividef(m1 * A.inv_bc1, den);
         if (A.lr_wd != 0.0f) pn -= A.lr_wd * pn;
         ep[z] = m1;
         sp[z] = m2;
