@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 22, help="elements per CPU thread")
+    ap.add_argument("--layout", default=None, help="SxR (shards x replicas) for N>1; default 1xN")
     return ap.parse_args()
 
 
@@ -153,12 +154,12 @@ def cpu_leg(args, n_threads: int, per_thread: int, reps: int = 1):
     return total / t, kind, sample
 
 
-def config_dict(args, n):
+def config_dict(args, n, layout=None):
     return {"workload": "OLMo-2-1B-shaped flat parameters (config 4), decoupled AdamW" if args.optimizer == "adamw"
             else "OLMo-2-1B-shaped flat parameters, DeMo-SGD",
             "params": args.params, "scheme": "demo", "chunk_size": args.chunk, "top_k": args.topk,
             "sign": bool(args.sign), "transfer_dtype": "fp32",
-            "layout": f"1x{n} (shard x replica)", "optimizer": args.optimizer,
+            "layout": f"{layout or f'1x{n}'} (shard x replica)", "optimizer": args.optimizer,
             "l2": "inputs (>= 4 x 5.9 GB) larger than L2 (126 MB)"}
 
 
@@ -211,23 +212,24 @@ def run_ours(args, rank, world, local_rank):
     gen.manual_seed(1234 + rank)
     grad = torch.empty(L, dtype=torch.float32, device=dev).normal_(0.0, 1e-3, generator=gen)
     params = torch.empty(L, dtype=torch.float32, device=dev).normal_(0.0, 0.02, generator=gen)
-    if args.optimizer == "adamw":
-        s1 = torch.zeros(L, dtype=torch.float32, device=dev)
-        s2 = torch.zeros(L, dtype=torch.float32, device=dev)
-    else:
-        s1 = torch.zeros(L, dtype=torch.float32, device=dev)  # momentum (in place)
-        s2 = None
+    s1 = s2 = None
+    if world == 1:
+        s1 = torch.zeros(L, dtype=torch.float32, device=dev)  # exp_avg, or the momentum (in place)
+        if args.optimizer == "adamw":
+            s2 = torch.zeros(L, dtype=torch.float32, device=dev)
     steps = C.c_uint64(0)
-    cap = int(lib.dmb_update_capacity(C.byref(c), L))
     distributed = world > 1
     if distributed:
         import torch.distributed as dist
 
-        own = torch.empty(cap, dtype=torch.uint8, device=dev)
-        gathered = torch.empty(world * cap, dtype=torch.uint8, device=dev)
-        hdr_own = _capi.Update()
-        hdr_own.body = own.data_ptr()
-        ups = (_capi.Update * world)()
+        from paper_2502_06728_b200.cluster import HybridCluster, Topology, groups_for
+
+        S, R = (int(v) for v in (args.layout or f"1x{world}").lower().split("x"))
+        assert S * R == world, f"layout {S}x{R} does not match {world} ranks"
+        topo = Topology(nodes=R, accels_per_node=S)
+        sg, rg = groups_for(topo, rank)
+        cluster = HybridCluster(topo, L, opt, cfg, params, rank, sg, rg)
+        del params
 
     def check(rc):
         if rc != 0:
@@ -243,22 +245,9 @@ def run_ours(args, rank, world, local_rank):
                 check(lib.dmb_step_sgd_local(ctx, grad.data_ptr(), s1.data_ptr(), s1.data_ptr(), params.data_ptr(),
                                              params.data_ptr(), L, C.byref(o), C.byref(c), step, 0, 1e-3, None, sp))
             return
-        # 1xN: prepare -> NCCL all-gather of fixed-size payloads -> merge + apply
-        if args.optimizer == "adamw":
-            check(lib.dmb_adamw_prepare(ctx, grad.data_ptr(), L, C.byref(c), step, 0, C.byref(hdr_own), None, sp))
-        else:
-            check(lib.dmb_demo_sgd_prepare(ctx, grad.data_ptr(), s1.data_ptr(), s1.data_ptr(), L, C.byref(o),
-                                           C.byref(c), step, 0, C.byref(hdr_own), None, None, sp))
-        dist.all_gather_into_tensor(gathered, own)
-        for r in range(world):
-            ups[r] = hdr_own
-            ups[r].body = gathered.data_ptr() + r * cap
-        if args.optimizer == "adamw":
-            check(lib.dmb_merge_apply_adamw(ctx, ups, world, rank, C.byref(c), params.data_ptr(), s1.data_ptr(),
-                                            s2.data_ptr(), C.byref(steps), grad.data_ptr(), L, step, C.byref(o),
-                                            1e-3, sp))
-        else:
-            check(lib.dmb_merge_apply_sgd(ctx, ups, world, C.byref(c), params.data_ptr(), None, L, step, 1e-3, sp))
+        # SxR: reduce-scatter in the shard group -> prepare -> NCCL all-gather of the
+        # payloads in the replica group -> rank-ordered merge + apply (cluster.cpp:171-232)
+        cluster.step(step, 1e-3, grad, check=False)
 
     def barrier():
         if distributed:
@@ -293,7 +282,8 @@ def run_ours(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms = total_ms / args.steps
-    value = world * L / (ms * 1e-3)
+    shard_len = cluster.spec.real_len if distributed else L
+    value = world * shard_len / (ms * 1e-3)  # parameters processed by all ranks per second
 
     # ---- roofline of the dominant kernel (the fused step at N=1) ----
     hbm, peak_kind = peaks()
@@ -301,9 +291,9 @@ def run_ours(args, rank, world, local_rank):
     if distributed:
         # prepare reads g (4); merge+apply reads g again + p/m/v r/w (28) + (1+R) payloads
         P_b = (args.topk / args.chunk) * 8
-        B_alg = (32 if args.optimizer == "adamw" else 24) + (1 + world) * P_b
+        B_alg = (32 if args.optimizer == "adamw" else 24) + (1 + cluster.topo.nodes) * P_b
     kern_ms = statistics.median(per_step)
-    achieved = B_alg * L / (kern_ms * 1e-3) / 1e9
+    achieved = B_alg * shard_len / (kern_ms * 1e-3) / 1e9
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -348,13 +338,16 @@ def run_ours(args, rank, world, local_rank):
             "metric": METRIC, "value": value, "unit": "params/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (N(0,1e-3^2) gradients, N(0,0.02^2) params)",
-            "config": config_dict(args, world),
+            "config": config_dict(args, world, args.layout),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
-                         "kernel": "demo_chunk_kernel<StepAdam>" if not distributed else "merge_apply",
+                         "kernel": ("demo_tc4_kernel<StepAdam> (tcgen05)" if args.optimizer == "adamw"
+                                    else "demo_tc_kernel<StepSgd> (tcgen05)") if not distributed
+                         else "whole step incl. NCCL all-gather",
                          "bytes_per_param": B_alg, "peak_source": peak_kind},
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
-            "per_gpu_params_per_s": L / (ms * 1e-3),
+            "per_gpu_params_per_s": shard_len / (ms * 1e-3),
+            "model_params_per_s": L / (ms * 1e-3),
         }
         print(json.dumps(line), flush=True)
 
@@ -373,6 +366,8 @@ def main():
 
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.layout is None and args.gpus != world:
+            args.gpus = world
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
