@@ -368,6 +368,7 @@ AdamScalars adam_scalars(const dmb_opt_cfg* o, uint64_t steps_after, double lr) 
   a.inv_bc2 = (float)(1.0 / bc2);
   a.eps = (float)o->adam_eps;
   a.lr = (float)lr;
+  a.lr_bc1 = (float)(lr / bc1);
   a.lr_wd = o->weight_decay != 0.0 ? (float)(lr * o->weight_decay) : 0.0f;
   return a;
 }

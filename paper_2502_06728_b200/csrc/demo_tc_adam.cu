@@ -1,0 +1,1033 @@
+// demo_tc_adam.cu -- warp-specialised tensor-core DeMo kernel for the decoupled-AdamW
+// paths at chunk size 64 (the bench headline: OLMo-1B-shaped FlexDeMo + AdamW on one B200).
+//
+// One persistent CTA per SM, tiles of 128 chunks (8192 parameters), three roles that
+// run concurrently on different tiles:
+//   select warps 0-7  (quad layout, tcgen05.ld/st 16x256b: 4 lanes per chunk, 2 chunks
+//                      per quad, column 8r + 2(lane%4) + b)
+//        - gradient tile t+1 (TMA, 128B swizzle) -> TF32 hi/lo + raw copy -> TMEM,
+//          ||x||_1 per chunk, require_finite
+//        - coefficients of tile t from TMEM -> TopK (radix select), certification against
+//          the FP64 oracle, exact FP64 re-derivation of what the FP32 bound cannot order,
+//          payload, W = wire - coef on the selection -> TMEM (TF32 hi/lo)
+//   apply warps 8-15  (slice layout, tcgen05.ld 32x32b: thread = chunk, 32 columns)
+//        - D = IDCT(W) and the raw gradient from TMEM, p / exp_avg / exp_avg_sq from the
+//          shared-memory staging tile (TMA), decoupled AdamW in place in the staging tile
+//   control warp 16   - every TMA load / store and every tcgen05.mma, in tile order:
+//                       forward C = X B^T and inverse D = W B in 3xTF32 (A from TMEM)
+// The optimizer state streams through shared memory with TMA bulk tensor copies, so the
+// HBM traffic of tile t overlaps the selection of tile t+1 without occupying registers.
+//
+// TMEM columns: C [0,64)  D [64,128)  X/W hi [128,192)  X/W lo [192,256)  raw gradient
+// ring of three tiles [256,448).  W reuses the X columns (X of t+1 is consumed by the
+// forward MMA before W of t is written; W of t by the inverse before X of t+2).
+//
+// Reference: transform.cpp:56-73, :127-147 (DCT, TopK, inverse); replicate.cpp:137-144,
+// :282-309 (conditioning, merge); optim.cpp:51-74 (decoupled AdamW).  Modes: StepAdam
+// (prepare + merge(R=1) + apply), MergeAdam (R gathered payloads + own indices -> apply),
+// EncodeAdam (payload only).  The one partial chunk at the shard end is handed to the
+// SIMT kernel through the fallback list.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cfloat>
+#include <cstring>
+#include <mutex>
+
+#include "dmb_internal.cuh"
+#include "tc_ptx.cuh"
+
+namespace dmb {
+namespace {
+
+using namespace ptx;
+
+constexpr int S = 64;
+constexpr int TM = 128;
+constexpr int kSelWarps = 8;
+constexpr int kAppWarps = 4;
+constexpr int kMmaWarp = kSelWarps + kAppWarps;  // gradient TMA + every tcgen05.mma
+constexpr int kMemWarp = kMmaWarp + 1;           // optimizer-state TMA loads / stores
+constexpr int THREADS = (kMemWarp + 1) * 32;
+
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(S >> 3) << 17) |
+                           ((uint32_t)(TM >> 4) << 24);
+
+constexpr uint32_t TILE = TM * S * 4;   // 32 KB
+constexpr uint32_t BOX = TILE / 2;      // one 32-column TMA box
+constexpr uint32_t BMAT = S * 128 * 2;  // 16 KB
+constexpr uint32_t OFF_BHI = 0;          // B[j][i]   forward B operand (K-major SW128)
+constexpr uint32_t OFF_BLO = BMAT;
+constexpr uint32_t OFF_BTHI = 2 * BMAT;  // B^T[i][j] inverse B operand
+constexpr uint32_t OFF_BTLO = 3 * BMAT;
+constexpr uint32_t OFF_G = 4 * BMAT;            // gradient tile (TMA, swizzled)
+constexpr uint32_t OFF_ST = OFF_G + TILE;       // p, exp_avg, exp_avg_sq staging tiles
+constexpr uint32_t OFF_SCR = OFF_ST + 3 * TILE; // merge: grids (8 x 4 KB); else: FP64 basis (XOR-swizzled)
+constexpr uint32_t SCR_WARP = 4096;
+constexpr int kCap = 32;                         // exact re-derivations per warp and tile
+constexpr uint32_t RES_WARP = kCap * 2 + 16;     // (row, column) keys + slots left per row
+constexpr uint32_t OFF_RES = OFF_SCR + kSelWarps * SCR_WARP;
+constexpr uint32_t OFF_BAR = OFF_RES + kSelWarps * RES_WARP;
+constexpr uint32_t SMEM_BYTES = OFF_BAR + 128;
+static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+
+constexpr uint32_t COL_C = 0, COL_D = 64, COL_XH = 128, COL_XL = 192, COL_G = 256;
+constexpr uint32_t TMEM_COLS = 512;
+
+constexpr float kEpsScale = 1.52587890625e-05f * 0.1767766952966369f * 1.01f;  // 2^-16 sqrt(2/64)
+
+__device__ __forceinline__ uint32_t sw_off(int r, int q) {  // 16-byte unit q of row r
+  return (uint32_t)(q >> 3) * (TM * 128u) + (uint32_t)r * 128u + ((uint32_t)((q & 7) ^ (r & 7)) << 4);
+}
+__device__ __forceinline__ uint32_t sw_off_b(int r, int q) {
+  return (uint32_t)(q >> 3) * (S * 128u) + (uint32_t)r * 128u + ((uint32_t)((q & 7) ^ (r & 7)) << 4);
+}
+// quad layout: element e (0..15) of a thread with slice s sits in column 8(e/2) + 2s + e%2
+__device__ __forceinline__ int qcol(int e, int s) { return 8 * (e >> 1) + 2 * s + (e & 1); }
+
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_2d_store(const CUtensorMap* map, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// 16 TMEM lanes x 64 columns: thread t gets lanes base + t/4 (regs 4r, 4r+1) and
+// base + 8 + t/4 (regs 4r+2, 4r+3) at columns 8r + 2(t%4) + {0, 1}
+__device__ __forceinline__ void ld_quad(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x8.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%"
+      "28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void st_quad(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.16x256b.x8.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%"
+      "29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+// two rows of 16 values <-> the 32 quad-layout registers
+__device__ __forceinline__ void unpack_rows(const uint32_t (&r)[32], float (&c0)[16], float (&c1)[16]) {
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    c0[e] = __uint_as_float(r[4 * (e >> 1) + (e & 1)]);
+    c1[e] = __uint_as_float(r[4 * (e >> 1) + 2 + (e & 1)]);
+  }
+}
+__device__ __forceinline__ void pack_rows(const float (&c0)[16], const float (&c1)[16], uint32_t (&r)[32]) {
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    r[4 * (e >> 1) + (e & 1)] = __float_as_uint(c0[e]);
+    r[4 * (e >> 1) + 2 + (e & 1)] = __float_as_uint(c1[e]);
+  }
+}
+
+__device__ __forceinline__ void evt(const ChunkArgs& a, bool who, uint32_t it, int id) {
+  if (a.dbg && who && blockIdx.x == 0 && it < 32) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg[it * 16 + id] = t;
+  }
+}
+
+__device__ __forceinline__ void evt_at(const ChunkArgs& a, bool who, uint32_t it, int slot) {
+  if (a.dbg && who && blockIdx.x == 0 && it < 32) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.dbg[512 + it * 32 + slot] = t;
+  }
+}
+
+__device__ __forceinline__ float quad_sumf(float v) {
+  v += __shfl_xor_sync(kFull, v, 1);
+  return v + __shfl_xor_sync(kFull, v, 2);
+}
+__device__ __forceinline__ int quad_sum(int v) {
+  v += __shfl_xor_sync(kFull, v, 1);
+  return v + __shfl_xor_sync(kFull, v, 2);
+}
+__device__ __forceinline__ float quad_min(float v) {
+  v = fminf(v, __shfl_xor_sync(kFull, v, 1));
+  return fminf(v, __shfl_xor_sync(kFull, v, 2));
+}
+__device__ __forceinline__ float quad_max(float v) {
+  v = fmaxf(v, __shfl_xor_sync(kFull, v, 1));
+  return fmaxf(v, __shfl_xor_sync(kFull, v, 2));
+}
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int src) {
+  return ((uint64_t)__shfl_sync(kFull, (uint32_t)(v >> 32), src) << 32) | (uint64_t)__shfl_sync(kFull, (uint32_t)v, src);
+}
+// this thread's 16 element bits -> the chunk's 64 column bits
+__device__ __forceinline__ uint64_t spread(uint32_t bits, int s) {
+  uint64_t m = 0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) m |= (uint64_t)((bits >> (2 * r)) & 3u) << (8 * r + 2 * s);
+  return m;
+}
+__device__ __forceinline__ uint32_t gather16(uint64_t m, int s) {  // inverse of spread
+  uint32_t b = 0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) b |= (uint32_t)((m >> (8 * r + 2 * s)) & 3u) << (2 * r);
+  return b;
+}
+
+__device__ __forceinline__ int count_ge16(const float (&c)[16], float t) {
+  int n0 = 0, n1 = 0, n2 = 0, n3 = 0;
+#pragma unroll
+  for (int j = 0; j < 16; j += 4) {
+    n0 += fabsf(c[j]) >= t;
+    n1 += fabsf(c[j + 1]) >= t;
+    n2 += fabsf(c[j + 2]) >= t;
+    n3 += fabsf(c[j + 3]) >= t;
+  }
+  return (n0 + n1) + (n2 + n3);
+}
+
+struct RowSel {
+  uint32_t T;
+  bool done, exact;
+};
+__device__ __forceinline__ RowSel row_start(const float (&c)[16], bool active, int& top) {
+  float mx = 0.f, mn = FLT_MAX;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    mx = fmaxf(mx, fabsf(c[j]));
+    mn = fminf(mn, fabsf(c[j]));
+  }
+  mx = quad_max(mx);
+  mn = quad_min(mn);
+  const uint32_t diff = __float_as_uint(mx) ^ __float_as_uint(mn);
+  top = diff ? 31 - __clz(diff) : -1;
+  RowSel r;
+  r.T = top >= 0 ? (__float_as_uint(mx) & ~((2u << top) - 1u)) : __float_as_uint(mx);
+  r.done = !active || top < 0;
+  r.exact = false;
+  return r;
+}
+__device__ __forceinline__ void row_step(RowSel& r, const float (&c)[16], int k, int b) {
+  const uint32_t cand = r.T | (1u << b);
+  const int cnt = quad_sum(count_ge16(c, __uint_as_float(cand)));
+  if (!r.done && cnt >= k) {
+    r.T = cand;
+    if (cnt == k) r.exact = r.done = true;
+  }
+}
+// final selection of a row from its threshold: everything above T, then the lowest
+// columns among the keys equal to T (ties toward the lower index)
+__device__ __forceinline__ uint32_t row_finish(const RowSel& r, const float (&c)[16], int k, int s, bool active,
+                                               bool any_tie) {
+  const float Tf = __uint_as_float(r.T);
+  uint32_t gt = 0, eq = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float m = fabsf(c[j]);
+    if (m > Tf) gt |= 1u << j;
+    if (m == Tf) eq |= 1u << j;
+  }
+  uint32_t sel = r.exact ? (gt | eq) : gt;
+  if (any_tie) {  // warp-uniform
+    const int gt_all = quad_sum(__popc(gt));
+    uint64_t eq64 = spread(eq, s);
+    eq64 |= shfl64(eq64, (threadIdx.x & 28) | ((threadIdx.x + 1) & 3));
+    eq64 |= shfl64(eq64, (threadIdx.x & 28) | ((threadIdx.x + 2) & 3));
+    if (!r.exact) {
+      uint64_t pick = 0, m = eq64;
+      for (int n = k - gt_all; n > 0 && m; --n) {
+        pick |= m & (~m + 1ull);
+        m &= m - 1ull;
+      }
+      sel = gt | gather16(pick, s);
+    }
+  }
+  return active ? sel : 0u;
+}
+
+
+// ---- bitonic TopK threshold (k = 8, 16, 32 of 64): the k-th largest |c| of a chunk held
+// by a quad (16 values per lane) from a local bitonic sort and merge-max steps across the
+// quad -- no data-dependent loop, every step independent compare-exchanges ----
+__device__ __forceinline__ void cas_desc(float& x, float& y) {
+  const float hi = fmaxf(x, y);
+  y = fminf(x, y);
+  x = hi;
+}
+__device__ __forceinline__ void sort16_desc(float (&a)[16]) {
+#pragma unroll
+  for (int size = 2; size <= 16; size <<= 1)
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int j = i ^ stride;
+        if (j > i) {
+          if ((i & size) == 0) cas_desc(a[i], a[j]);
+          else cas_desc(a[j], a[i]);
+        }
+      }
+}
+template <int N>
+__device__ __forceinline__ void merge_desc(float (&a)[16]) {  // bitonic a[0..N) -> descending
+#pragma unroll
+  for (int stride = N >> 1; stride > 0; stride >>= 1)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int j = i ^ stride;
+      if (j > i) cas_desc(a[i], a[j]);
+    }
+}
+__device__ __forceinline__ float kth_bitonic(const float (&c)[16], int k) {
+  const int lane = threadIdx.x & 31;
+  float a[16], p[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) a[j] = fabsf(c[j]);
+  sort16_desc(a);
+  float m = FLT_MAX;
+  if (k == 32) {
+    // lanes (s, s^1) -> one sorted 32: the even lane keeps the top half, the odd the bottom
+    const bool upper = (lane & 1) == 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) p[i] = __shfl_sync(kFull, a[15 - i], lane ^ 1);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = upper ? fmaxf(a[i], p[i]) : fminf(a[i], p[i]);
+    merge_desc<16>(a);
+    // top 32 of 64: sorted pair (0,1) against the reversed pair (3,2)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) p[i] = __shfl_sync(kFull, a[15 - i], lane ^ 3);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) m = fminf(m, fmaxf(a[i], p[i]));
+    m = fminf(m, __shfl_xor_sync(kFull, m, 1));
+  } else if (k == 16) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) p[i] = __shfl_sync(kFull, a[15 - i], lane ^ 1);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = fmaxf(a[i], p[i]);  // top 16 of the pair (bitonic)
+    merge_desc<16>(a);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) p[i] = __shfl_sync(kFull, a[15 - i], lane ^ 2);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) m = fminf(m, fmaxf(a[i], p[i]));
+  } else {  // k == 8
+#pragma unroll
+    for (int i = 0; i < 8; ++i) p[i] = __shfl_sync(kFull, a[7 - i], lane ^ 1);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fmaxf(a[i], p[i]);
+    merge_desc<8>(a);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) p[i] = __shfl_sync(kFull, a[7 - i], lane ^ 2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m = fminf(m, fmaxf(a[i], p[i]));
+  }
+  return m;
+}
+__device__ __forceinline__ bool bitonic_k(int k) { return k == 8 || k == 16 || k == 32; }
+
+// wire conditioning specialised per transfer format (replicate.cpp:137-144)
+enum : int { kWireSign = 0, kWireF16 = 1, kWireF32 = 2 };
+template <int WIRE>
+__device__ __forceinline__ float cond_w(float c) {
+  if (WIRE == kWireSign) return c != 0.0f ? copysignf(1.0f, c) : 0.0f;  // NaN never reaches the wire
+  if (WIRE == kWireF16) return __half2float(__float2half_rn(c));
+  return c;
+}
+// exact TF32 split: hi keeps the top 10 mantissa bits, lo = x - hi is exact in FP32
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+
+struct TensorMaps {
+  CUtensorMap g, p_in, ea_in, es_in, p_out, ea_out, es_out;
+};
+
+template <ChunkMode MODE, int WIRE>
+__global__ void __maxnreg__(128)
+    demo_tc_adam_kernel(const ChunkArgs a, const __grid_constant__ TensorMaps maps) {
+  constexpr bool kEncodeOnly = MODE == ChunkMode::EncodeAdam;
+  constexpr bool kMerge = MODE == ChunkMode::MergeAdam;
+
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023u) != 0u) __trap();
+  uint64_t* bar_g = reinterpret_cast<uint64_t*>(smem + OFF_BAR);  // gradient tile landed (TMA)
+  uint64_t* bar_x = bar_g + 1;  // X in TMEM, gradient stage consumed (8 select warps)
+  uint64_t* bar_f = bar_x + 1;  // forward DCT done (tcgen05.commit)
+  uint64_t* bar_w = bar_f + 1;  // W in TMEM (8 select warps)
+  uint64_t* bar_i = bar_w + 1;  // inverse DCT done (tcgen05.commit)
+  uint64_t* bar_s = bar_i + 1;  // optimizer state staged (TMA)
+  uint64_t* bar_a = bar_s + 1;  // AdamW written into the staging tile (8 apply warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_a + 1);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+
+  if (!kEncodeOnly && step_failed(a.status)) return;
+
+  for (int u = tid; u < S * 16; u += THREADS) {
+    const int r = u >> 4, q = u & 15;
+    *reinterpret_cast<float4*>(smem + OFF_BHI + sw_off_b(r, q)) = *reinterpret_cast<const float4*>(a.basis.Bhi + r * S + 4 * q);
+    *reinterpret_cast<float4*>(smem + OFF_BLO + sw_off_b(r, q)) = *reinterpret_cast<const float4*>(a.basis.Blo + r * S + 4 * q);
+    *reinterpret_cast<float4*>(smem + OFF_BTHI + sw_off_b(r, q)) = *reinterpret_cast<const float4*>(a.basis.BThi + r * S + 4 * q);
+    *reinterpret_cast<float4*>(smem + OFF_BTLO + sw_off_b(r, q)) = *reinterpret_cast<const float4*>(a.basis.BTlo + r * S + 4 * q);
+  }
+  if (!kMerge) {  // the FP64 basis of the exact re-derivation: element (j, i) at j*64 + (i ^ (j & 15))
+    double* b64 = reinterpret_cast<double*>(smem + OFF_SCR);
+    for (int u = tid; u < S * S; u += THREADS) {
+      const int j = u >> 6, i = u & 63;
+      b64[j * S + (i ^ (j & 15))] = a.basis.B64[u];
+    }
+  }
+  if (tid == 0) {
+    mbar_init(bar_g, 1);
+    mbar_init(bar_x, kSelWarps);
+    mbar_init(bar_f, 1);
+    mbar_init(bar_w, kSelWarps);
+    mbar_init(bar_i, 1);
+    mbar_init(bar_s, 1);
+    mbar_init(bar_a, kAppWarps);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, TMEM_COLS);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const uint64_t len = a.geo.len;
+  const uint64_t nchunks = a.geo.nchunks;
+  const uint64_t nfull = len / S;  // rows of the tensor maps; a partial last chunk goes to the SIMT fix-up
+  const uint64_t ntiles = (nchunks + TM - 1) / TM;
+  const uint64_t G = gridDim.x;
+  const int k = a.geo.k;
+  const bool full_band = k == S;
+  uint64_t tile = blockIdx.x;
+
+  auto load_state = [&](uint64_t t) {  // one thread
+    mbar_arrive_expect_tx(bar_s, 3 * TILE);
+    const CUtensorMap* m[3] = {&maps.p_in, &maps.ea_in, &maps.es_in};
+#pragma unroll
+    for (int v = 0; v < 3; ++v) {
+      tma_2d(smem + OFF_ST + v * TILE, m[v], 0, (int)(t * TM), bar_s);
+      tma_2d(smem + OFF_ST + v * TILE + BOX, m[v], 32, (int)(t * TM), bar_s);
+    }
+  };
+  // The two control warps stay converged: every lane runs the loop and the waits, lane 0
+  // issues the TMA / tcgen05 operations.
+  if (warp == kMemWarp) {
+    // ===== state warp: p / exp_avg / exp_avg_sq through the staging tile =====
+    if (!kEncodeOnly) {
+      if (tile < ntiles && lane == 0) load_state(tile);
+      for (uint32_t it = 0; tile < ntiles; tile += G, ++it) {
+        mbar_wait(bar_a, it & 1);  // AdamW of this tile written into the staging tile
+        if (lane == 0) {
+          const CUtensorMap* m[3] = {&maps.p_out, &maps.ea_out, &maps.es_out};
+#pragma unroll
+          for (int v = 0; v < 3; ++v) {
+            tma_2d_store(m[v], 0, (int)(tile * TM), smem + OFF_ST + v * TILE);
+            tma_2d_store(m[v], 32, (int)(tile * TM), smem + OFF_ST + v * TILE + BOX);
+          }
+          bulk_commit();
+          bulk_wait_read();  // the staging tile may be refilled
+          if (tile + G < ntiles) load_state(tile + G);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) bulk_wait_all();
+      __syncwarp();
+    }
+    goto teardown;
+  }
+
+  if (warp == kMmaWarp) {
+    // ===== MMA warp: gradient TMA and tcgen05.mma issue, in tile order =====
+    const uint32_t s_base = smem_u32(smem);
+    auto load_g = [&](uint64_t t) {
+      if (lane == 0) {
+        mbar_arrive_expect_tx(bar_g, TILE);
+        tma_2d(smem + OFF_G, &maps.g, 0, (int)(t * TM), bar_g);
+        tma_2d(smem + OFF_G + BOX, &maps.g, 32, (int)(t * TM), bar_g);
+      }
+      __syncwarp();
+    };
+    // D = A(TMEM: hi, lo) x B(smem hi, lo) in 3xTF32 over K = 64
+    auto issue = [&](uint32_t d, uint32_t bh, uint32_t bl, uint64_t* bar) {
+      tc_fence_after();
+      if (lane == 0) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t bo = (uint32_t)(kk >> 2) * (S * 128u) + (uint32_t)(kk & 3) * 32u;
+          const uint32_t ahi = tmem + COL_XH + 8u * kk, alo = tmem + COL_XL + 8u * kk;
+          mma_tf32_ts(d, ahi, desc_sw128(s_base + bh + bo), IDESC, kk > 0 ? 1u : 0u);
+          mma_tf32_ts(d, ahi, desc_sw128(s_base + bl + bo), IDESC, 1u);
+          mma_tf32_ts(d, alo, desc_sw128(s_base + bh + bo), IDESC, 1u);
+        }
+        mma_commit(bar);
+      }
+      __syncwarp();
+    };
+    if (tile < ntiles) {
+      load_g(tile);
+      mbar_wait(bar_x, 0);
+      issue(tmem + COL_C, OFF_BHI, OFF_BLO, bar_f);
+      if (tile + G < ntiles) load_g(tile + G);
+    }
+    for (uint32_t it = 0; tile < ntiles; tile += G, ++it) {
+      const uint64_t t1 = tile + G;
+      if (t1 < ntiles) {
+        mbar_wait(bar_x, (it + 1) & 1);  // X of t+1 in TMEM; the gradient stage is free
+        issue(tmem + COL_C, OFF_BHI, OFF_BLO, bar_f);
+        if (t1 + G < ntiles) load_g(t1 + G);
+      }
+      if (!kEncodeOnly) {
+        mbar_wait(bar_w, it & 1);
+        evt(a, tid == 32 * kMmaWarp, it, 14);
+        if (it > 0) mbar_wait(bar_a, (it - 1) & 1);  // D of t-1 read by the apply warps
+        evt(a, tid == 32 * kMmaWarp, it, 15);
+        issue(tmem + COL_D, OFF_BTHI, OFF_BTLO, bar_i);
+      }
+    }
+    goto teardown;
+  }
+
+  if (warp >= kSelWarps) {
+    if (kEncodeOnly) goto teardown;
+    // ===== apply warps: thread = chunk 32 (warp % 4) + lane, all 64 columns in two halves =====
+    const int trow = 32 * (warp & 3) + lane;
+    const uint32_t tl = (uint32_t)(32 * (warp & 3)) << 16;
+    const AdamScalars A = a.adam;
+    for (uint32_t it = 0; tile < ntiles; tile += G, ++it) {
+      evt(a, tid == 32 * kSelWarps, it, 10);
+      mbar_wait_spin(bar_i, it & 1);
+      evt(a, tid == 32 * kSelWarps, it, 11);
+      mbar_wait(bar_s, it & 1);
+      tc_fence_after();
+      evt(a, tid == 32 * kSelWarps, it, 12);
+      bool deferred = false;
+#pragma unroll 1
+      for (int h = 0; h < 4; ++h) {  // 16 columns at a time: every load of the quarter in flight together
+        float d[16], g[16];
+        tmem_ld16(tmem + tl + COL_D + 16 * h, d);
+        tmem_ld16(tmem + tl + COL_G + 64 * (it % 3) + 16 * h, g);
+        float4 p4[4], e4[4], s4[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t off = OFF_ST + sw_off(trow, 4 * h + e);
+          p4[e] = *reinterpret_cast<const float4*>(smem + off);
+          e4[e] = *reinterpret_cast<const float4*>(smem + off + TILE);
+          s4[e] = *reinterpret_cast<const float4*>(smem + off + 2 * TILE);
+        }
+        tmem_ld_wait();
+        // (tcgen05.ld is warp-collective: every lane loads, a deferred row only skips its writes)
+        if (h == 0) deferred = isnan(d[0]);  // handed to the FP64 fix-up: state stays as loaded
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float* pz = &p4[e].x;
+          float* ez = &e4[e].x;
+          float* sz = &s4[e].x;
+#pragma unroll
+          for (int z = 0; z < 4; ++z) {
+            const float gp = full_band ? d[4 * e + z] : g[4 * e + z] + d[4 * e + z];  // g - local_q + Q (optim.cpp:65)
+            const float m1 = A.beta1 * ez[z] + A.one_minus_beta1 * gp;
+            const float m2 = A.beta2 * sz[z] + A.one_minus_beta2 * gp * gp;
+            float sq;
+            asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(m2 * A.inv_bc2));
+            float pn = pz[z] - __fdividef(m1 * A.lr_bc1, sq + A.eps);
+            pn -= A.lr_wd * pn;  // decoupled weight decay (0 when disabled)
+            ez[z] = m1;
+            sz[z] = m2;
+            pz[z] = pn;
+          }
+        }
+        if (!deferred) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t off = OFF_ST + sw_off(trow, 4 * h + e);
+            *reinterpret_cast<float4*>(smem + off) = p4[e];
+            *reinterpret_cast<float4*>(smem + off + TILE) = e4[e];
+            *reinterpret_cast<float4*>(smem + off + 2 * TILE) = s4[e];
+          }
+        }
+      }
+      tc_fence_before();
+      fence_proxy_async_smem();  // generic writes -> the TMA store
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_a);
+      evt(a, tid == 32 * kSelWarps, it, 13);
+    }
+    goto teardown;
+  }
+
+  {
+    // ===== select warps: quad layout, rows base + lane/4 and base + 8 + lane/4 =====
+    const int s = lane & 3;
+    const int base = 32 * (warp & 3) + 16 * (warp >> 2);
+    const int row0 = base + (lane >> 2), row1 = row0 + 8;  // tile rows
+    const uint32_t tq = (uint32_t)base << 16;
+    const int dtype = a.geo.dtype;
+    const bool sign_mode = a.geo.sign_mode;
+    const bool need_signs = sign_mode || dtype == DMB_TERNARY;
+    const uint64_t nvals = nchunks * (uint64_t)k;
+    const bool partial_last = (len % S) != 0;
+    uint8_t* scr = smem + OFF_SCR + warp * SCR_WARP;
+
+    // b: gradient tile -> TMEM (hi, lo, raw) + ||x||_1 of both rows
+    auto front = [&](uint64_t t, uint32_t n, float& l1a, float& l1b, uint32_t it) {
+      mbar_wait(bar_g, n & 1);
+      evt(a, tid == 0, it, 3);
+      float x0[16], x1[16];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {  // columns 8r + 2s, +1: 16-byte unit 2r + s/2, offset 8 (s & 1)
+        const float2 v0 = *reinterpret_cast<const float2*>(smem + OFF_G + sw_off(row0, 2 * r + (s >> 1)) + 8 * (s & 1));
+        const float2 v1 = *reinterpret_cast<const float2*>(smem + OFF_G + sw_off(row1, 2 * r + (s >> 1)) + 8 * (s & 1));
+        x0[2 * r] = v0.x;
+        x0[2 * r + 1] = v0.y;
+        x1[2 * r] = v1.x;
+        x1[2 * r + 1] = v1.y;
+      }
+      float a0 = 0.f, a1 = 0.f;
+      bool fin = true;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        a0 += fabsf(x0[e]);
+        a1 += fabsf(x1[e]);
+        fin = fin && isfinite(x0[e]) && isfinite(x1[e]);
+      }
+      if (!fin) {  // require_finite (vec.cpp:7-16): the lowest offending index wins
+        for (int e = 0; e < 16; ++e) {
+          if (!isfinite(x0[e])) latch_bad(a.status, (t * TM + row0) * S + qcol(e, s));
+          if (!isfinite(x1[e])) latch_bad(a.status, (t * TM + row1) * S + qcol(e, s));
+        }
+      }
+      l1a = quad_sumf(a0);
+      l1b = quad_sumf(a1);
+      uint32_t r[32];
+      pack_rows(x0, x1, r);
+      st_quad(tmem + tq + COL_G + 64 * (n % 3), r);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const float h0 = tf32_hi(x0[e]), h1 = tf32_hi(x1[e]);
+        x0[e] -= h0;
+        x1[e] -= h1;
+        r[4 * (e >> 1) + (e & 1)] = __float_as_uint(h0);
+        r[4 * (e >> 1) + 2 + (e & 1)] = __float_as_uint(h1);
+      }
+      st_quad(tmem + tq + COL_XH, r);
+      pack_rows(x0, x1, r);
+      st_quad(tmem + tq + COL_XL, r);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_x);
+    };
+
+    float l1n0 = 0.f, l1n1 = 0.f;
+    if (tile < ntiles) front(tile, 0, l1n0, l1n1, 99);
+    for (uint32_t it = 0; tile < ntiles; tile += G, ++it) {
+      const uint64_t t1 = tile + G;
+      const bool has_next = t1 < ntiles;
+      const uint64_t trow0 = tile * TM;
+      const uint64_t r0 = trow0 + row0, r1 = trow0 + row1;
+      const bool act0 = r0 < nfull, act1 = r1 < nfull;
+      if (partial_last && s == 0 && (r0 == nchunks - 1 || r1 == nchunks - 1)) {
+        const unsigned slot = atomicAdd(a.fb_count, 1u);
+        a.fb_list[slot] = (uint32_t)(nchunks - 1);
+      }
+      const float l10 = l1n0, l11 = l1n1;
+      evt(a, tid == 0, it, 0);
+      evt_at(a, lane == 0, it, 24 + warp);
+      mbar_wait_spin(bar_f, it & 1);
+      evt(a, tid == 0, it, 1);
+      tc_fence_after();
+      float c0[16], c1[16];
+      {
+        uint32_t r[32];
+        ld_quad(tmem + tq + COL_C, r);
+        tmem_ld_wait();
+        unpack_rows(r, c0, c1);
+      }
+      if (!kEncodeOnly && it > 0) mbar_wait_spin(bar_i, (it - 1) & 1);  // W of t-1 consumed: X columns free
+      evt(a, tid == 0, it, 2);
+      if (has_next) front(t1, it + 1, l1n0, l1n1, it);
+      evt(a, tid == 0, it, 4);
+
+      uint32_t sel0 = 0, sel1 = 0;
+      bool def0 = false, def1 = false;
+      if (!kMerge) {
+        // ---- TopK of both rows (warp-uniform trip count) ----
+        if (full_band) {
+          sel0 = act0 ? 0xffffu : 0u;
+          sel1 = act1 ? 0xffffu : 0u;
+        } else if (bitonic_k(k)) {
+          const float T0 = kth_bitonic(c0, k), T1 = kth_bitonic(c1, k);
+          RowSel q0{__float_as_uint(T0), true, false}, q1{__float_as_uint(T1), true, false};
+          q0.exact = quad_sum(count_ge16(c0, T0)) == k;
+          q1.exact = quad_sum(count_ge16(c1, T1)) == k;
+          const bool any_tie = __any_sync(kFull, (act0 && !q0.exact) || (act1 && !q1.exact));
+          sel0 = row_finish(q0, c0, k, s, act0, any_tie);
+          sel1 = row_finish(q1, c1, k, s, act1, any_tie);
+        } else {
+          int top0, top1;
+          RowSel q0 = row_start(c0, act0, top0), q1 = row_start(c1, act1, top1);
+          const int top_w = (int)__reduce_max_sync(kFull, (unsigned)(max(top0, top1) + 1)) - 1;
+#pragma unroll 1
+          for (int b = top_w; b >= 0; --b) {
+            if (__all_sync(kFull, q0.done && q1.done)) break;
+            row_step(q0, c0, k, b);
+            row_step(q1, c1, k, b);
+          }
+          const bool any_tie = __any_sync(kFull, (act0 && !q0.exact) || (act1 && !q1.exact));
+          sel0 = row_finish(q0, c0, k, s, act0, any_tie);
+          sel1 = row_finish(q1, c1, k, s, act1, any_tie);
+        }
+        evt(a, tid == 0, it, 5);
+        evt_at(a, lane == 0, it, 8 + warp);
+        // ---- certification against the FP64 oracle (the FP32 bound decides most chunks) ----
+        uint32_t amb0 = 0, cin0 = 0, amb1 = 0, cin1 = 0;
+        bool res0 = false, res1 = false;
+        auto certify = [&](const float (&c)[16], uint32_t sel, float l1, bool act, bool& need, uint32_t& amb,
+                           uint32_t& cin) {
+          float kth = FLT_MAX, nxt = 0.f;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float m = fabsf(c[j]);
+            if ((sel >> j) & 1u) kth = fminf(kth, m);
+            else nxt = fmaxf(nxt, m);
+          }
+          kth = quad_min(kth);
+          nxt = quad_max(nxt);
+          const float eps = kEpsScale * l1;
+          if (!act) return;
+          const bool sel_unc = !full_band && !(kth - nxt > 2.0f * eps);
+          const bool sign_unc = need_signs && !(kth > eps);
+          need = !isnan(l1) && (sel_unc || sign_unc || a.force_fp64);
+          if (!need) return;
+          const float hi_b = a.force_fp64 ? FLT_MAX : nxt + 2.0f * eps;
+          const float lo_b = a.force_fp64 ? 0.0f : kth - 2.0f * eps;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float m = fabsf(c[j]);
+            const bool is_amb = full_band ? (m <= eps || a.force_fp64) : (m >= lo_b && m <= hi_b);
+            if (is_amb) amb |= 1u << j;
+            else if (!full_band && m > hi_b) cin |= 1u << j;
+          }
+        };
+        certify(c0, sel0, l10, act0, res0, amb0, cin0);
+        certify(c1, sel1, l11, act1, res1, amb1, cin1);
+        if (__any_sync(kFull, res0 || res1)) {
+          // Exact resolution: every ambiguous key of the warp's uncertain chunks gets its FP64
+          // coefficient, one key per lane, products summed from 0.0 in the oracle's order
+          // (transform.cpp:56-63); each chunk then takes its remaining slots among them by
+          // exact |value|, ties toward the lower column.  More keys than the warp's scratch
+          // holds (force_fp64 tests) send the chunks whole to the FP64 fix-up kernel.
+          uint16_t* plist = reinterpret_cast<uint16_t*>(smem + OFF_RES + warp * RES_WARP);
+          const double* b64 = reinterpret_cast<const double*>(smem + OFF_SCR);
+          const int n0 = res0 ? __popc(amb0) : 0, n1 = res1 ? __popc(amb1) : 0;
+          int incl = n0 + n1;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += v;
+          }
+          const int total = __shfl_sync(kFull, incl, 31);
+          const int start0 = incl - n0 - n1, start1 = start0 + n0;
+          if (total <= kCap) {
+            // key of each ambiguous coefficient: (row in the warp, column); slots left per row
+            uint8_t* rneed = reinterpret_cast<uint8_t*>(plist + kCap);
+            const int need0 = k - quad_sum(res0 ? __popc(cin0) : 0), need1 = k - quad_sum(res1 ? __popc(cin1) : 0);
+            if (s == 0) {
+              rneed[lane >> 2] = (uint8_t)need0;
+              rneed[(lane >> 2) + 8] = (uint8_t)need1;
+            }
+            int p0 = start0, p1 = start1;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              if (res0 && ((amb0 >> e) & 1u)) plist[p0++] = (uint16_t)(((lane >> 2) << 8) | qcol(e, s));
+              if (res1 && ((amb1 >> e) & 1u)) plist[p1++] = (uint16_t)((((lane >> 2) + 8) << 8) | qcol(e, s));
+            }
+            __syncwarp();
+            // lane q: exact coefficient of key q; the row's raw gradient arrives from the quad
+            // that holds it in TMEM, 16 values per round
+            uint32_t xr[32];
+            ld_quad(tmem + tq + COL_G + 64 * (it % 3), xr);
+            tmem_ld_wait();
+            const bool mine = lane < total;
+            const int key = mine ? plist[lane] : 0;
+            const int lr = key >> 8, j = key & 63;
+            const int src = 4 * (lr & 7), hi_row = lr >> 3;
+            const double* br = b64 + j * S;
+            const int sw = j & 15;
+            double acc = 0.0;
+#pragma unroll
+            for (int i0 = 0; i0 < S; i0 += 16) {
+              double prod[16];
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const int i = i0 + u;
+                const int reg = 4 * (i >> 3) + (i & 1);
+                const uint32_t v0 = __shfl_sync(kFull, xr[reg], src + ((i & 7) >> 1));
+                const uint32_t v1 = __shfl_sync(kFull, xr[reg + 2], src + ((i & 7) >> 1));
+                prod[u] = __dmul_rn(br[i ^ sw], (double)__uint_as_float(hi_row ? v1 : v0));
+              }
+#pragma unroll
+              for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, prod[u]);
+            }
+            // rank among the ambiguous keys of the same row: larger |value| first, then the
+            // lower column; the row's remaining slots go to the best ranks
+            const double v = fabs(acc);
+            int rank = 0;
+#pragma unroll 8
+            for (int q = 0; q < kCap; ++q) {
+              const double u = fabs(__shfl_sync(kFull, acc, q));
+              const int kq = __shfl_sync(kFull, key, q);
+              rank += q < total && (kq >> 8) == lr && (u > v || (u == v && (kq & 63) < j));
+            }
+            const bool chosen = mine && rank < (int)rneed[lr];
+            // back to the quads: exact values and decisions of their ambiguous coefficients
+            auto settle = [&](float (&c)[16], uint32_t& sel, uint32_t amb, bool res, int p) {
+              uint32_t pick = 0;
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                const bool am = res && ((amb >> e) & 1u);
+                const int from = am ? p : lane;
+                const double xv = __shfl_sync(kFull, acc, from);
+                const bool ch = __shfl_sync(kFull, chosen, from);
+                if (am) {
+                  c[e] = (float)xv;
+                  if (ch) pick |= 1u << e;
+                  ++p;
+                }
+              }
+              if (res && !full_band) sel = (sel & ~amb) | pick;
+            };
+            settle(c0, sel0, amb0, res0, start0);
+            settle(c1, sel1, amb1, res1, start1);
+          } else {
+            def0 = res0;
+            def1 = res1;
+          }
+          __syncwarp();
+        }
+        // a chunk handed to the FP64 fix-up kernel keeps a NaN-tagged W row so the apply
+        // warps leave its state as loaded
+        if (s == 0 && (def0 || def1)) {
+          const unsigned slot = atomicAdd(a.fb_count, (unsigned)def0 + (unsigned)def1);
+          if (def0) a.fb_list[slot] = (uint32_t)r0;
+          if (def1) a.fb_list[slot + (unsigned)def0] = (uint32_t)r1;
+        }
+        evt(a, tid == 0, it, 6);
+        evt_at(a, lane == 0, it, 16 + warp);
+        // ---- payload: indices ascending, then values (replicate.cpp:316-356) ----
+        if (a.body) {
+          const uint64_t q0m = spread(sel0, s), q1m = spread(sel1, s);
+          uint64_t all0 = q0m, all1 = q1m;
+          all0 |= shfl64(all0, (lane & 28) | ((lane + 1) & 3));
+          all1 |= shfl64(all1, (lane & 28) | ((lane + 1) & 3));
+          all0 |= shfl64(all0, (lane & 28) | ((lane + 2) & 3));
+          all1 |= shfl64(all1, (lane & 28) | ((lane + 2) & 3));
+          uint32_t* idx = reinterpret_cast<uint32_t*>(a.body);
+          uint8_t* vals = a.body + nvals * 4;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int col = qcol(e, s);
+            const uint64_t below = (1ull << col) - 1ull;
+            if (act0 && !def0 && ((sel0 >> e) & 1u)) {
+              const uint64_t t = r0 * (uint64_t)k + __popcll(all0 & below);
+              idx[t] = (uint32_t)col;
+              store_wire_value(vals, t, cond_w<WIRE>(c0[e]), dtype);
+            }
+            if (act1 && !def1 && ((sel1 >> e) & 1u)) {
+              const uint64_t t = r1 * (uint64_t)k + __popcll(all1 & below);
+              idx[t] = (uint32_t)col;
+              store_wire_value(vals, t, cond_w<WIRE>(c1[e]), dtype);
+            }
+          }
+        }
+      } else {
+        // ---- merge: the R gathered payloads in member order (replicate.cpp:282-300) into
+        // this warp's grid [16][64] (column XOR (row & 7) << 3), own selection ----
+        float* grid = reinterpret_cast<float*>(scr);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) grid[lane + 32 * j] = 0.0f;
+        __syncwarp();
+        const uint8_t* own_body = a.in.body[a.own_rank];
+        uint64_t own0 = 0, own1 = 0;
+        for (int lr = 0; lr < 16; ++lr) {
+          const uint64_t row = trow0 + base + lr;
+          if (row >= nfull) break;  // warp-uniform
+          for (int rr = 0; rr < a.in.R; ++rr) {
+            const uint32_t* idx_r = reinterpret_cast<const uint32_t*>(a.in.body[rr]) + row * (uint64_t)k;
+            const uint8_t* val_r = a.in.body[rr] + nvals * 4;
+            for (int t = lane; t < k; t += 32) {  // a chunk's indices are distinct inside one replica
+              const uint32_t j = __ldg(idx_r + t);
+              if (j < (uint32_t)S) grid[lr * S + (j ^ ((lr & 7) << 3))] += load_wire_value(val_r, row * (uint64_t)k + t, dtype);
+              else atomicExch(&a.status->protocol_error, 1u);
+            }
+            __syncwarp();
+          }
+          const uint32_t* idx_o = reinterpret_cast<const uint32_t*>(own_body) + row * (uint64_t)k;
+          uint64_t om = 0;
+          for (int t = lane; t < k; t += 32) om |= 1ull << (__ldg(idx_o + t) & 63u);
+          om = ((uint64_t)__reduce_or_sync(kFull, (uint32_t)(om >> 32)) << 32) | __reduce_or_sync(kFull, (uint32_t)om);
+          if (lr == (lane >> 2)) own0 = om;
+          if (lr == (lane >> 2) + 8) own1 = om;
+        }
+        __syncwarp();
+        sel0 = act0 ? gather16(own0, s) : 0u;
+        sel1 = act1 ? gather16(own1, s) : 0u;
+      }
+
+      if (!kEncodeOnly) {
+        // ---- W = wire - coef on the selection (Q - local_q of this tile) -> TMEM ----
+        const float invR = kMerge ? 1.0f / (float)a.in.R : 1.0f;
+        const float* grid = reinterpret_cast<const float*>(scr);
+        const int l0 = lane >> 2, l1 = l0 + 8;
+        float w0[16], w1[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int col = qcol(e, s);
+          const bool on0 = (sel0 >> e) & 1u, on1 = (sel1 >> e) & 1u;
+          float v0, v1;
+          if (kMerge) {
+            v0 = grid[l0 * S + (col ^ ((l0 & 7) << 3))] * invR - ((on0 && !full_band) ? c0[e] : 0.0f);
+            v1 = grid[l1 * S + (col ^ ((l1 & 7) << 3))] * invR - ((on1 && !full_band) ? c1[e] : 0.0f);
+          } else {
+            v0 = full_band ? cond_w<WIRE>(c0[e]) : (on0 ? cond_w<WIRE>(c0[e]) - c0[e] : 0.0f);
+            v1 = full_band ? cond_w<WIRE>(c1[e]) : (on1 ? cond_w<WIRE>(c1[e]) - c1[e] : 0.0f);
+          }
+          w0[e] = def0 ? __int_as_float(0x7fc00000) : (act0 ? v0 : 0.0f);
+          w1[e] = def1 ? __int_as_float(0x7fc00000) : (act1 ? v1 : 0.0f);
+        }
+        evt(a, tid == 0, it, 7);
+        if (has_next) mbar_wait_spin(bar_f, (it + 1) & 1);  // X of t+1 consumed: the columns take W
+        evt(a, tid == 0, it, 8);
+        tc_fence_after();
+        uint32_t r[32];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float h0 = tf32_hi(w0[e]), h1 = tf32_hi(w1[e]);
+          w0[e] -= h0;
+          w1[e] -= h1;
+          r[4 * (e >> 1) + (e & 1)] = __float_as_uint(h0);
+          r[4 * (e >> 1) + 2 + (e & 1)] = __float_as_uint(h1);
+        }
+        st_quad(tmem + tq + COL_XH, r);
+        pack_rows(w0, w1, r);
+        st_quad(tmem + tq + COL_XL, r);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_w);
+      }
+      evt(a, tid == 0, it, 9);
+      evt_at(a, lane == 0, it, warp);
+    }
+  }
+
+teardown:
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tmem, TMEM_COLS);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// [rows = whole chunks][64 floats], boxes of 128 rows x 32 columns, 128-byte swizzle
+void tile_map(CUtensorMap* m, const float* base, uint64_t rows) {
+  const cuuint64_t dims[2] = {(cuuint64_t)S, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)S * 4};
+  const cuuint32_t box[2] = {32, TM};
+  const cuuint32_t estr[2] = {1, 1};
+  encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
+template <ChunkMode MODE, int WIRE>
+void launch_wire(const ChunkArgs& a, const TensorMaps& maps, cudaStream_t stream) {
+  auto kern = demo_tc_adam_kernel<MODE, WIRE>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t ntiles = (a.geo.nchunks + TM - 1) / TM;
+  const unsigned grid = (unsigned)(ntiles < (uint64_t)sms ? (ntiles ? ntiles : 1) : sms);
+  kern<<<grid, THREADS, SMEM_BYTES, stream>>>(a, maps);
+}
+template <ChunkMode MODE>
+void launch_mode(const ChunkArgs& a, const TensorMaps& maps, cudaStream_t stream) {
+  if (a.geo.sign_mode || a.geo.dtype == DMB_TERNARY) launch_wire<MODE, kWireSign>(a, maps, stream);
+  else if (a.geo.dtype == DMB_FP16) launch_wire<MODE, kWireF16>(a, maps, stream);
+  else launch_wire<MODE, kWireF32>(a, maps, stream);
+}
+
+}  // namespace
+
+bool tc3_supported(ChunkMode mode, const ChunkArgs& a) {
+  if (a.geo.s != S || a.basis.Bhi == nullptr || encode_fn() == nullptr) return false;
+  if (!(mode == ChunkMode::StepAdam || mode == ChunkMode::MergeAdam || mode == ChunkMode::EncodeAdam))
+    return false;
+  if (a.local_q || a.m_accum || a.q_out) return false;  // inspection outputs: generic kernels
+  if (a.geo.len / S == 0) return false;                 // the tensor maps need one whole chunk
+  if (mode == ChunkMode::MergeAdam && (a.in.R < 1 || a.own_rank < 0 || a.own_rank >= a.in.R)) return false;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  if (!al(a.g)) return false;
+  if (mode == ChunkMode::EncodeAdam) return true;
+  return al(a.p_in) && al(a.p_out) && al(a.ea_in) && al(a.ea_out) && al(a.es_in) && al(a.es_out);
+}
+
+void launch_tc3_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) {
+  count_launches(1);
+  TensorMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  const uint64_t rows = a.geo.len / S;
+  tile_map(&maps.g, a.g, rows);
+  if (mode != ChunkMode::EncodeAdam) {
+    tile_map(&maps.p_in, a.p_in, rows);
+    tile_map(&maps.ea_in, a.ea_in, rows);
+    tile_map(&maps.es_in, a.es_in, rows);
+    tile_map(&maps.p_out, a.p_out, rows);
+    tile_map(&maps.ea_out, a.ea_out, rows);
+    tile_map(&maps.es_out, a.es_out, rows);
+  }
+  switch (mode) {
+    case ChunkMode::StepAdam: launch_mode<ChunkMode::StepAdam>(a, maps, stream); break;
+    case ChunkMode::MergeAdam: launch_mode<ChunkMode::MergeAdam>(a, maps, stream); break;
+    case ChunkMode::EncodeAdam: launch_mode<ChunkMode::EncodeAdam>(a, maps, stream); break;
+    default: break;
+  }
+}
+
+}  // namespace dmb

@@ -95,6 +95,7 @@ struct AdamScalars {
   float beta1, one_minus_beta1, beta2, one_minus_beta2;
   float inv_bc1, inv_bc2;  // 1/(1 - beta^t), std::pow on the host (optim.cpp:62-63)
   float eps, lr, lr_wd;    // lr * weight_decay (0 disables, optim.cpp:71)
+  float lr_bc1;            // lr / (1 - beta1^t)
 };
 
 // ---------------------------------------------------------------------------
