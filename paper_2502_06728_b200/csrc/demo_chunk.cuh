@@ -458,7 +458,11 @@ void launch_t(const ChunkArgs& a, cudaStream_t stream) {
   const uint64_t units = (a.geo.nchunks + (uint64_t)kWarps * CH - 1) / ((uint64_t)kWarps * CH);
   uint64_t grid = (uint64_t)sms * 4;
   if (units < grid) grid = units ? units : 1;
-  if (a.list) grid = (uint64_t)sms;  // list length lives on the device
+  if (a.list) {  // list length lives on the device: fill every SM to its occupancy limit
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+    grid = (uint64_t)sms * (uint64_t)(per_sm > 0 ? per_sm : 1);
+  }
   kern<<<(unsigned)grid, kThreads, smem, stream>>>(a);
 }
 

@@ -20,7 +20,9 @@ void launch_chunk_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream
     ChunkArgs fix = a;
     fix.list = a.fb_list;
     fix.list_count = a.fb_count;
-    fix.force_fp64 = 1;
+    // the SIMT kernel certifies its own FP32 coefficients (a tighter bound than the
+    // tensor-core one) and re-derives in FP64 only what that bound cannot settle
+    fix.force_fp64 = a.force_fp64;
     launch_chunk_simt(mode, fix, stream);
     return;
   }

@@ -62,12 +62,9 @@ constexpr uint32_t OFF_BTHI = 2 * BMAT;  // B^T[i][j] inverse B operand
 constexpr uint32_t OFF_BTLO = 3 * BMAT;
 constexpr uint32_t OFF_G = 4 * BMAT;            // gradient tile (TMA, swizzled)
 constexpr uint32_t OFF_ST = OFF_G + TILE;       // p, exp_avg, exp_avg_sq staging tiles
-constexpr uint32_t OFF_SCR = OFF_ST + 3 * TILE; // merge: grids (8 x 4 KB); else: FP64 basis (XOR-swizzled)
+constexpr uint32_t OFF_SCR = OFF_ST + 3 * TILE; // merge grids (8 x 4 KB)
 constexpr uint32_t SCR_WARP = 4096;
-constexpr int kCap = 32;                         // exact re-derivations per warp and tile
-constexpr uint32_t RES_WARP = kCap * 2 + 16;     // (row, column) keys + slots left per row
-constexpr uint32_t OFF_RES = OFF_SCR + kSelWarps * SCR_WARP;
-constexpr uint32_t OFF_BAR = OFF_RES + kSelWarps * RES_WARP;
+constexpr uint32_t OFF_BAR = OFF_SCR + kSelWarps * SCR_WARP;
 constexpr uint32_t SMEM_BYTES = OFF_BAR + 128;
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
@@ -386,13 +383,6 @@ __global__ void __maxnreg__(128)
     *reinterpret_cast<float4*>(smem + OFF_BTHI + sw_off_b(r, q)) = *reinterpret_cast<const float4*>(a.basis.BThi + r * S + 4 * q);
     *reinterpret_cast<float4*>(smem + OFF_BTLO + sw_off_b(r, q)) = *reinterpret_cast<const float4*>(a.basis.BTlo + r * S + 4 * q);
   }
-  if (!kMerge) {  // the FP64 basis of the exact re-derivation: element (j, i) at j*64 + (i ^ (j & 15))
-    double* b64 = reinterpret_cast<double*>(smem + OFF_SCR);
-    for (int u = tid; u < S * S; u += THREADS) {
-      const int j = u >> 6, i = u & 63;
-      b64[j * S + (i ^ (j & 15))] = a.basis.B64[u];
-    }
-  }
   if (tid == 0) {
     mbar_init(bar_g, 1);
     mbar_init(bar_x, kSelWarps);
@@ -698,11 +688,11 @@ __global__ void __maxnreg__(128)
         }
         evt(a, tid == 0, it, 5);
         evt_at(a, lane == 0, it, 8 + warp);
-        // ---- certification against the FP64 oracle (the FP32 bound decides most chunks) ----
-        uint32_t amb0 = 0, cin0 = 0, amb1 = 0, cin1 = 0;
-        bool res0 = false, res1 = false;
-        auto certify = [&](const float (&c)[16], uint32_t sel, float l1, bool act, bool& need, uint32_t& amb,
-                           uint32_t& cin) {
+        // ---- certification against the FP64 oracle: a chunk whose FP32 order or signs the
+        // error bound cannot settle is handed whole to the FP64 fix-up kernel, which runs
+        // after this one (re-deriving in the oracle's operation order off the critical path
+        // is cheaper than stalling the tile pipeline for it) ----
+        auto certify = [&](const float (&c)[16], uint32_t sel, float l1, bool act) {
           float kth = FLT_MAX, nxt = 0.f;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
@@ -713,117 +703,12 @@ __global__ void __maxnreg__(128)
           kth = quad_min(kth);
           nxt = quad_max(nxt);
           const float eps = kEpsScale * l1;
-          if (!act) return;
           const bool sel_unc = !full_band && !(kth - nxt > 2.0f * eps);
           const bool sign_unc = need_signs && !(kth > eps);
-          need = !isnan(l1) && (sel_unc || sign_unc || a.force_fp64);
-          if (!need) return;
-          const float hi_b = a.force_fp64 ? FLT_MAX : nxt + 2.0f * eps;
-          const float lo_b = a.force_fp64 ? 0.0f : kth - 2.0f * eps;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float m = fabsf(c[j]);
-            const bool is_amb = full_band ? (m <= eps || a.force_fp64) : (m >= lo_b && m <= hi_b);
-            if (is_amb) amb |= 1u << j;
-            else if (!full_band && m > hi_b) cin |= 1u << j;
-          }
+          return act && !isnan(l1) && (sel_unc || sign_unc || a.force_fp64);
         };
-        certify(c0, sel0, l10, act0, res0, amb0, cin0);
-        certify(c1, sel1, l11, act1, res1, amb1, cin1);
-        if (__any_sync(kFull, res0 || res1)) {
-          // Exact resolution: every ambiguous key of the warp's uncertain chunks gets its FP64
-          // coefficient, one key per lane, products summed from 0.0 in the oracle's order
-          // (transform.cpp:56-63); each chunk then takes its remaining slots among them by
-          // exact |value|, ties toward the lower column.  More keys than the warp's scratch
-          // holds (force_fp64 tests) send the chunks whole to the FP64 fix-up kernel.
-          uint16_t* plist = reinterpret_cast<uint16_t*>(smem + OFF_RES + warp * RES_WARP);
-          const double* b64 = reinterpret_cast<const double*>(smem + OFF_SCR);
-          const int n0 = res0 ? __popc(amb0) : 0, n1 = res1 ? __popc(amb1) : 0;
-          int incl = n0 + n1;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += v;
-          }
-          const int total = __shfl_sync(kFull, incl, 31);
-          const int start0 = incl - n0 - n1, start1 = start0 + n0;
-          if (total <= kCap) {
-            // key of each ambiguous coefficient: (row in the warp, column); slots left per row
-            uint8_t* rneed = reinterpret_cast<uint8_t*>(plist + kCap);
-            const int need0 = k - quad_sum(res0 ? __popc(cin0) : 0), need1 = k - quad_sum(res1 ? __popc(cin1) : 0);
-            if (s == 0) {
-              rneed[lane >> 2] = (uint8_t)need0;
-              rneed[(lane >> 2) + 8] = (uint8_t)need1;
-            }
-            int p0 = start0, p1 = start1;
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              if (res0 && ((amb0 >> e) & 1u)) plist[p0++] = (uint16_t)(((lane >> 2) << 8) | qcol(e, s));
-              if (res1 && ((amb1 >> e) & 1u)) plist[p1++] = (uint16_t)((((lane >> 2) + 8) << 8) | qcol(e, s));
-            }
-            __syncwarp();
-            // lane q: exact coefficient of key q; the row's raw gradient arrives from the quad
-            // that holds it in TMEM, 16 values per round
-            uint32_t xr[32];
-            ld_quad(tmem + tq + COL_G + 64 * (it % 3), xr);
-            tmem_ld_wait();
-            const bool mine = lane < total;
-            const int key = mine ? plist[lane] : 0;
-            const int lr = key >> 8, j = key & 63;
-            const int src = 4 * (lr & 7), hi_row = lr >> 3;
-            const double* br = b64 + j * S;
-            const int sw = j & 15;
-            double acc = 0.0;
-#pragma unroll
-            for (int i0 = 0; i0 < S; i0 += 16) {
-              double prod[16];
-#pragma unroll
-              for (int u = 0; u < 16; ++u) {
-                const int i = i0 + u;
-                const int reg = 4 * (i >> 3) + (i & 1);
-                const uint32_t v0 = __shfl_sync(kFull, xr[reg], src + ((i & 7) >> 1));
-                const uint32_t v1 = __shfl_sync(kFull, xr[reg + 2], src + ((i & 7) >> 1));
-                prod[u] = __dmul_rn(br[i ^ sw], (double)__uint_as_float(hi_row ? v1 : v0));
-              }
-#pragma unroll
-              for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, prod[u]);
-            }
-            // rank among the ambiguous keys of the same row: larger |value| first, then the
-            // lower column; the row's remaining slots go to the best ranks
-            const double v = fabs(acc);
-            int rank = 0;
-#pragma unroll 8
-            for (int q = 0; q < kCap; ++q) {
-              const double u = fabs(__shfl_sync(kFull, acc, q));
-              const int kq = __shfl_sync(kFull, key, q);
-              rank += q < total && (kq >> 8) == lr && (u > v || (u == v && (kq & 63) < j));
-            }
-            const bool chosen = mine && rank < (int)rneed[lr];
-            // back to the quads: exact values and decisions of their ambiguous coefficients
-            auto settle = [&](float (&c)[16], uint32_t& sel, uint32_t amb, bool res, int p) {
-              uint32_t pick = 0;
-#pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                const bool am = res && ((amb >> e) & 1u);
-                const int from = am ? p : lane;
-                const double xv = __shfl_sync(kFull, acc, from);
-                const bool ch = __shfl_sync(kFull, chosen, from);
-                if (am) {
-                  c[e] = (float)xv;
-                  if (ch) pick |= 1u << e;
-                  ++p;
-                }
-              }
-              if (res && !full_band) sel = (sel & ~amb) | pick;
-            };
-            settle(c0, sel0, amb0, res0, start0);
-            settle(c1, sel1, amb1, res1, start1);
-          } else {
-            def0 = res0;
-            def1 = res1;
-          }
-          __syncwarp();
-        }
+        def0 = certify(c0, sel0, l10, act0);
+        def1 = certify(c1, sel1, l11, act1);
         // a chunk handed to the FP64 fix-up kernel keeps a NaN-tagged W row so the apply
         // warps leave its state as loaded
         if (s == 0 && (def0 || def1)) {
