@@ -765,27 +765,41 @@ __global__ void __maxnreg__(128)
 #pragma unroll
         for (int j = 0; j < 32; ++j) grid[lane + 32 * j] = 0.0f;
         __syncwarp();
-        const uint8_t* own_body = a.in.body[a.own_rank];
+        // the warp's 16 rows of one replica are loaded together (one memory latency per
+        // replica and 32 frequencies), then added in member order
+        const uint64_t wrow = trow0 + base;
+        const int nrows = wrow < nfull ? (nfull - wrow < 16 ? (int)(nfull - wrow) : 16) : 0;  // warp-uniform
         uint64_t own0 = 0, own1 = 0;
-        for (int lr = 0; lr < 16; ++lr) {
-          const uint64_t row = trow0 + base + lr;
-          if (row >= nfull) break;  // warp-uniform
-          for (int rr = 0; rr < a.in.R; ++rr) {
-            const uint32_t* idx_r = reinterpret_cast<const uint32_t*>(a.in.body[rr]) + row * (uint64_t)k;
-            const uint8_t* val_r = a.in.body[rr] + nvals * 4;
-            for (int t = lane; t < k; t += 32) {  // a chunk's indices are distinct inside one replica
-              const uint32_t j = __ldg(idx_r + t);
-              if (j < (uint32_t)S) grid[lr * S + (j ^ ((lr & 7) << 3))] += load_wire_value(val_r, row * (uint64_t)k + t, dtype);
-              else atomicExch(&a.status->protocol_error, 1u);
+        for (int rr = 0; rr < a.in.R; ++rr) {
+          const uint32_t* idx_r = reinterpret_cast<const uint32_t*>(a.in.body[rr]) + wrow * (uint64_t)k;
+          const uint8_t* val_r = a.in.body[rr] + nvals * 4;
+          const bool own_r = rr == a.own_rank;
+          for (int t0 = 0; t0 < k; t0 += 32) {
+            const int t = t0 + lane;
+            uint32_t jj[16];
+            float vv[16];
+#pragma unroll
+            for (int lr = 0; lr < 16; ++lr) {
+              const bool ok = lr < nrows && t < k;
+              jj[lr] = ok ? __ldg(idx_r + lr * k + t) : 0xffffffffu;
+              vv[lr] = ok ? load_wire_value(val_r, (wrow + lr) * (uint64_t)k + t, dtype) : 0.0f;
             }
-            __syncwarp();
+#pragma unroll
+            for (int lr = 0; lr < 16; ++lr) {
+              const uint32_t j = jj[lr];
+              // a chunk's indices are distinct inside one replica: no two lanes collide
+              if (j < (uint32_t)S) grid[lr * S + (j ^ ((lr & 7) << 3))] += vv[lr];
+              else if (j != 0xffffffffu) atomicExch(&a.status->protocol_error, 1u);
+              if (own_r) {
+                const uint64_t bit = j < (uint32_t)S ? 1ull << j : 0ull;
+                const uint64_t om = ((uint64_t)__reduce_or_sync(kFull, (uint32_t)(bit >> 32)) << 32) |
+                                    __reduce_or_sync(kFull, (uint32_t)bit);
+                if (lr == (lane >> 2)) own0 |= om;
+                if (lr == (lane >> 2) + 8) own1 |= om;
+              }
+            }
           }
-          const uint32_t* idx_o = reinterpret_cast<const uint32_t*>(own_body) + row * (uint64_t)k;
-          uint64_t om = 0;
-          for (int t = lane; t < k; t += 32) om |= 1ull << (__ldg(idx_o + t) & 63u);
-          om = ((uint64_t)__reduce_or_sync(kFull, (uint32_t)(om >> 32)) << 32) | __reduce_or_sync(kFull, (uint32_t)om);
-          if (lr == (lane >> 2)) own0 = om;
-          if (lr == (lane >> 2) + 8) own1 = om;
+          __syncwarp();
         }
         __syncwarp();
         sel0 = act0 ? gather16(own0, s) : 0u;
