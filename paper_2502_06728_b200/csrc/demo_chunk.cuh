@@ -182,9 +182,9 @@ __global__ void __launch_bounds__(kThreads) demo_chunk_kernel(const ChunkArgs a)
 
   const uint64_t warps_total = (uint64_t)gridDim.x * kWarps;
   const bool list_mode = a.list != nullptr;
-  const uint64_t n_units = list_mode ? (uint64_t)*a.list_count : nchunks;
+  const uint64_t n_units = list_mode ? (uint64_t)*a.list_count : nchunks - a.first_chunk;
   for (uint64_t u0 = ((uint64_t)blockIdx.x * kWarps + warp) * CH; u0 < n_units; u0 += warps_total * CH) {
-    const uint64_t c0 = list_mode ? (uint64_t)a.list[u0] : u0;  // list mode: CH == 1
+    const uint64_t c0 = list_mode ? (uint64_t)a.list[u0] : a.first_chunk + u0;  // list mode: CH == 1
     float x[CH][E];    // encode: v (m_acc or g); merge-adam: g
     float gv[CH][E];   // raw gradient (adam paths)
     float Q[CH][E];    // merged update
@@ -322,8 +322,18 @@ __global__ void __launch_bounds__(kThreads) demo_chunk_kernel(const ChunkArgs a)
           }
         }
 
+        // one-rank AdamW step without a local_q output: g' = g - local_q + Q needs only
+        // IDCT(wire - coef) over the selection, one sparse inverse instead of two
+        const bool fused_w = MODE == ChunkMode::StepAdam && !a.local_q && k < s;
         // local_q (unsigned coefficients, SPEC: sign never touches local state)
-        if (k == s) {
+        if (fused_w) {
+          float wd[E];
+#pragma unroll
+          for (int e = 0; e < E; ++e) wd[e] = sel[e] ? wv[e] - csel[e] : 0.0f;
+          sparse_inverse<E>(wd, sel, B, s, Q[ch]);
+#pragma unroll
+          for (int e = 0; e < E; ++e) lq[ch][e] = 0.0f;
+        } else if (k == s) {
 #pragma unroll
           for (int e = 0; e < E; ++e) lq[ch][e] = x[ch][e];  // exact copy, transform.cpp:119-125
         } else {
@@ -344,7 +354,7 @@ __global__ void __launch_bounds__(kThreads) demo_chunk_kernel(const ChunkArgs a)
             if (in[ch][e]) a.local_q[gi] = lq[ch][e];
           }
         }
-        if (kStep) {
+        if (kStep && !fused_w) {
           // merge of a one-member group: grid = conditioned values / 1, then IDCT
           bool nz[E];
 #pragma unroll
@@ -455,7 +465,7 @@ void launch_t(const ChunkArgs& a, cudaStream_t stream) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const uint64_t units = (a.geo.nchunks + (uint64_t)kWarps * CH - 1) / ((uint64_t)kWarps * CH);
+  const uint64_t units = (a.geo.nchunks - a.first_chunk + (uint64_t)kWarps * CH - 1) / ((uint64_t)kWarps * CH);
   uint64_t grid = (uint64_t)sms * 4;
   if (units < grid) grid = units ? units : 1;
   if (a.list) {  // list length lives on the device: fill every SM to its occupancy limit

@@ -12,11 +12,23 @@ bool tc_enabled() {
 }
 
 void launch_chunk_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) {
-  const bool tc3 = tc_enabled() && a.fb_list && a.fb_count && tc3_supported(mode, a);
-  if (tc3 || (tc_enabled() && a.fb_list && a.fb_count && tc_supported(mode, a))) {
+  if (tc_enabled() && a.fb_list && a.fb_count && tc3_supported(mode, a)) {
+    // warp-specialised tensor-core kernel; the chunks its FP32 bound cannot certify are
+    // re-derived exactly by the FP64 fix-up kernel; a partial last chunk (its own
+    // length and basis) goes through the SIMT kernel
     cudaMemsetAsync(a.fb_count, 0, sizeof(unsigned), stream);
-    if (tc3) launch_tc3_kernel(mode, a, stream);
-    else launch_tc_kernel(mode, a, stream);
+    launch_tc3_kernel(mode, a, stream);
+    launch_fix64_kernel(mode, a, stream);
+    if (a.geo.len % a.geo.s) {
+      ChunkArgs tail = a;
+      tail.first_chunk = a.geo.nchunks - 1;
+      launch_chunk_simt(mode, tail, stream);
+    }
+    return;
+  }
+  if (tc_enabled() && a.fb_list && a.fb_count && tc_supported(mode, a)) {
+    cudaMemsetAsync(a.fb_count, 0, sizeof(unsigned), stream);
+    launch_tc_kernel(mode, a, stream);
     ChunkArgs fix = a;
     fix.list = a.fb_list;
     fix.list_count = a.fb_count;

@@ -65,7 +65,8 @@ constexpr uint32_t OFF_ST = OFF_G + TILE;       // p, exp_avg, exp_avg_sq stagin
 constexpr uint32_t OFF_SCR = OFF_ST + 3 * TILE; // merge grids (8 x 4 KB)
 constexpr uint32_t SCR_WARP = 4096;
 constexpr uint32_t OFF_BAR = OFF_SCR + kSelWarps * SCR_WARP;
-constexpr uint32_t SMEM_BYTES = OFF_BAR + 128;
+constexpr uint32_t OFF_L1 = OFF_BAR + 128;      // ||x||_1 per chunk, two tiles
+constexpr uint32_t SMEM_BYTES = OFF_L1 + 2 * TM * 4;
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
 constexpr uint32_t COL_C = 0, COL_D = 64, COL_XH = 128, COL_XL = 192, COL_G = 256;
@@ -372,13 +373,16 @@ __global__ void __maxnreg__(128)
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023u) != 0u) __trap();
   uint64_t* bar_g = reinterpret_cast<uint64_t*>(smem + OFF_BAR);  // gradient tile landed (TMA)
-  uint64_t* bar_x = bar_g + 1;  // X in TMEM, gradient stage consumed (8 select warps)
+  uint64_t* bar_x = bar_g + 1;  // X in TMEM, gradient stage consumed (apply warps)
   uint64_t* bar_f = bar_x + 1;  // forward DCT done (tcgen05.commit)
-  uint64_t* bar_w = bar_f + 1;  // W in TMEM (8 select warps)
+  uint64_t* bar_w = bar_f + 1;  // W in TMEM (select warps)
   uint64_t* bar_i = bar_w + 1;  // inverse DCT done (tcgen05.commit)
   uint64_t* bar_s = bar_i + 1;  // optimizer state staged (TMA)
-  uint64_t* bar_a = bar_s + 1;  // AdamW written into the staging tile (8 apply warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_a + 1);
+  uint64_t* bar_a = bar_s + 1;  // AdamW written into the staging tile (apply warps)
+  uint64_t* bar_c = bar_a + 1;  // coefficient tile read out of TMEM (select warps)
+  uint64_t* bar_l = bar_c + 1;  // [2] ||x||_1 of tile n in l1buf[n & 1] (apply warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_l + 2);
+  float* l1buf = reinterpret_cast<float*>(smem + OFF_L1);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -395,7 +399,10 @@ __global__ void __maxnreg__(128)
   }
   if (tid == 0) {
     mbar_init(bar_g, 1);
-    mbar_init(bar_x, kSelWarps);
+    mbar_init(bar_x, kAppWarps);
+    mbar_init(bar_c, kSelWarps);
+    mbar_init(&bar_l[0], kAppWarps);
+    mbar_init(&bar_l[1], kAppWarps);
     mbar_init(bar_f, 1);
     mbar_init(bar_w, kSelWarps);
     mbar_init(bar_i, 1);
@@ -496,6 +503,7 @@ __global__ void __maxnreg__(128)
       const uint64_t t1 = tile + G;
       if (t1 < ntiles) {
         mbar_wait(bar_x, (it + 1) & 1);  // X of t+1 in TMEM; the gradient stage is free
+        mbar_wait(bar_c, it & 1);        // C of t read out by the select warps
         issue(tmem + COL_C, OFF_BHI, OFF_BLO, bar_f);
         if (t1 + G < ntiles) load_g(t1 + G);
       }
@@ -511,14 +519,78 @@ __global__ void __maxnreg__(128)
   }
 
   if (warp >= kSelWarps) {
-    if (kEncodeOnly) goto teardown;
-    // ===== apply warps: thread = chunk 32 (warp % 4) + lane, all 64 columns in two halves =====
+    // ===== apply warps: thread = chunk 32 (warp % 4) + lane (tcgen05 32x32b layout) =====
+    // (1) the gradient tile two ahead: smem (TMA) -> TF32 hi / lo + raw copy -> TMEM,
+    //     ||x||_1 per chunk, require_finite;  (2) AdamW of this tile.
     const int trow = 32 * (warp & 3) + lane;
     const uint32_t tl = (uint32_t)(32 * (warp & 3)) << 16;
     const AdamScalars A = a.adam;
+    auto front = [&](uint64_t t, uint32_t n) {
+      mbar_wait(bar_g, n & 1);
+      float l1 = 0.f;
+      bool fin = true;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        float x[16], hi[16];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float4 v = *reinterpret_cast<const float4*>(smem + OFF_G + sw_off(trow, 4 * h + e));
+          x[4 * e] = v.x;
+          x[4 * e + 1] = v.y;
+          x[4 * e + 2] = v.z;
+          x[4 * e + 3] = v.w;
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          l1 += fabsf(x[e]);
+          fin = fin && isfinite(x[e]);
+        }
+        tmem_st16(tmem + tl + COL_G + 64 * (n % 3) + 16 * h, x);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          hi[e] = tf32_hi(x[e]);
+          x[e] -= hi[e];
+        }
+        tmem_st16(tmem + tl + COL_XH + 16 * h, hi);
+        tmem_st16(tmem + tl + COL_XL + 16 * h, x);
+      }
+      if (!fin) {  // require_finite (vec.cpp:7-16): the lowest offending index wins
+        const float* gs = reinterpret_cast<const float*>(smem + OFF_G);
+        for (int col = 0; col < S; ++col) {
+          const float v = *reinterpret_cast<const float*>(smem + OFF_G + sw_off(trow, col >> 2) + 4 * (col & 3));
+          if (!isfinite(v)) {
+            latch_bad(a.status, (t * TM + trow) * S + col);
+            break;
+          }
+        }
+        (void)gs;
+      }
+      l1buf[(n & 1) * TM + trow] = l1;
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(bar_x);
+        mbar_arrive(&bar_l[n & 1]);
+      }
+    };
+    if (tile < ntiles) front(tile, 0);
+    if (tile + G < ntiles) {
+      mbar_wait(bar_f, 0);  // X of the first tile consumed by its forward DCT
+      front(tile + G, 1);
+    }
     for (uint32_t it = 0; tile < ntiles; tile += G, ++it) {
+      if (tile + 2 * G < ntiles) {
+        // the X columns are free once the inverse of this tile (or, encode only, the
+        // forward of the next) has read them
+        if (!kEncodeOnly) mbar_wait(bar_i, it & 1);
+        else mbar_wait(bar_f, (it + 1) & 1);
+        tc_fence_after();
+        front(tile + 2 * G, it + 2);
+      }
+      if (kEncodeOnly) continue;
       evt(a, tid == 32 * kSelWarps, it, 10);
-      mbar_wait_spin(bar_i, it & 1);
+      mbar_wait(bar_i, it & 1);
       evt(a, tid == 32 * kSelWarps, it, 11);
       mbar_wait(bar_s, it & 1);
       tc_fence_after();
@@ -588,75 +660,17 @@ __global__ void __maxnreg__(128)
     const bool sign_mode = a.geo.sign_mode;
     const bool need_signs = sign_mode || dtype == DMB_TERNARY;
     const uint64_t nvals = nchunks * (uint64_t)k;
-    const bool partial_last = (len % S) != 0;
     uint8_t* scr = smem + OFF_SCR + warp * SCR_WARP;
 
-    // b: gradient tile -> TMEM (hi, lo, raw) + ||x||_1 of both rows
-    auto front = [&](uint64_t t, uint32_t n, float& l1a, float& l1b, uint32_t it) {
-      mbar_wait(bar_g, n & 1);
-      evt(a, tid == 0, it, 3);
-      float x0[16], x1[16];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {  // columns 8r + 2s, +1: 16-byte unit 2r + s/2, offset 8 (s & 1)
-        const float2 v0 = *reinterpret_cast<const float2*>(smem + OFF_G + sw_off(row0, 2 * r + (s >> 1)) + 8 * (s & 1));
-        const float2 v1 = *reinterpret_cast<const float2*>(smem + OFF_G + sw_off(row1, 2 * r + (s >> 1)) + 8 * (s & 1));
-        x0[2 * r] = v0.x;
-        x0[2 * r + 1] = v0.y;
-        x1[2 * r] = v1.x;
-        x1[2 * r + 1] = v1.y;
-      }
-      float a0 = 0.f, a1 = 0.f;
-      bool fin = true;
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        a0 += fabsf(x0[e]);
-        a1 += fabsf(x1[e]);
-        fin = fin && isfinite(x0[e]) && isfinite(x1[e]);
-      }
-      if (!fin) {  // require_finite (vec.cpp:7-16): the lowest offending index wins
-        for (int e = 0; e < 16; ++e) {
-          if (!isfinite(x0[e])) latch_bad(a.status, (t * TM + row0) * S + qcol(e, s));
-          if (!isfinite(x1[e])) latch_bad(a.status, (t * TM + row1) * S + qcol(e, s));
-        }
-      }
-      l1a = quad_sumf(a0);
-      l1b = quad_sumf(a1);
-      uint32_t r[32];
-      pack_rows(x0, x1, r);
-      st_quad(tmem + tq + COL_G + 64 * (n % 3), r);
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const float h0 = tf32_hi(x0[e]), h1 = tf32_hi(x1[e]);
-        x0[e] -= h0;
-        x1[e] -= h1;
-        r[4 * (e >> 1) + (e & 1)] = __float_as_uint(h0);
-        r[4 * (e >> 1) + 2 + (e & 1)] = __float_as_uint(h1);
-      }
-      st_quad(tmem + tq + COL_XH, r);
-      pack_rows(x0, x1, r);
-      st_quad(tmem + tq + COL_XL, r);
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_x);
-    };
-
-    float l1n0 = 0.f, l1n1 = 0.f;
-    if (tile < ntiles) front(tile, 0, l1n0, l1n1, 99);
     for (uint32_t it = 0; tile < ntiles; tile += G, ++it) {
       const uint64_t t1 = tile + G;
       const bool has_next = t1 < ntiles;
       const uint64_t trow0 = tile * TM;
       const uint64_t r0 = trow0 + row0, r1 = trow0 + row1;
       const bool act0 = r0 < nfull, act1 = r1 < nfull;
-      if (partial_last && s == 0 && (r0 == nchunks - 1 || r1 == nchunks - 1)) {
-        const unsigned slot = atomicAdd(a.fb_count, 1u);
-        a.fb_list[slot] = (uint32_t)(nchunks - 1);
-      }
-      const float l10 = l1n0, l11 = l1n1;
       evt(a, tid == 0, it, 0);
       evt_at(a, lane == 0, it, 24 + warp);
-      mbar_wait_spin(bar_f, it & 1);
+      mbar_wait(bar_f, it & 1);
       evt(a, tid == 0, it, 1);
       tc_fence_after();
       float c0[16], c1[16];
@@ -666,9 +680,11 @@ __global__ void __maxnreg__(128)
         tmem_ld_wait();
         unpack_rows(r, c0, c1);
       }
-      if (!kEncodeOnly && it > 0) mbar_wait_spin(bar_i, (it - 1) & 1);  // W of t-1 consumed: X columns free
-      evt(a, tid == 0, it, 2);
-      if (has_next) front(t1, it + 1, l1n0, l1n1, it);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_c);  // the forward of the next tile may overwrite C
+      mbar_wait(&bar_l[it & 1], (it >> 1) & 1);
+      const float l10 = l1buf[(it & 1) * TM + row0], l11 = l1buf[(it & 1) * TM + row1];
       evt(a, tid == 0, it, 4);
 
       uint32_t sel0 = 0, sel1 = 0;
@@ -828,7 +844,7 @@ __global__ void __maxnreg__(128)
           w1[e] = def1 ? __int_as_float(0x7fc00000) : (act1 ? v1 : 0.0f);
         }
         evt(a, tid == 0, it, 7);
-        if (has_next) mbar_wait_spin(bar_f, (it + 1) & 1);  // X of t+1 consumed: the columns take W
+        if (has_next) mbar_wait(bar_f, (it + 1) & 1);  // X of t+1 consumed: the columns take W
         evt(a, tid == 0, it, 8);
         tc_fence_after();
         uint32_t r[32];
@@ -858,6 +874,147 @@ teardown:
   __syncthreads();
   tc_fence_after();
   if (warp == 0) tmem_dealloc(tmem, TMEM_COLS);
+}
+
+// ---------------------------------------------------------------------------
+// FP64 fix-up of the full chunks the tensor-core kernel could not certify (fb_list): one
+// warp per chunk, lane j holds coefficients j and j+32.  The coefficients are re-derived
+// in the oracle's operation order (acc = 0; acc = acc + B[j][i]*x_i, ascending i, no FMA:
+// transform.cpp:56-63) from the FP64 basis in shared memory, the TopK is exact on them
+// (ties toward the lower index, transform.cpp:127-133), then the chunk gets the same wire
+// values, payload and W = wire - coef -> D = IDCT(W) -> AdamW as in the main kernel (whose
+// apply warps left this chunk's state untouched).
+constexpr int kFixWarps = 8;
+constexpr uint32_t FIX_SMEM = S * S * 8 + S * S * 4;  // FP64 basis (swizzled) + FP32 basis
+
+template <ChunkMode MODE, int WIRE>
+__global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkArgs a) {
+  constexpr bool kEncodeOnly = MODE == ChunkMode::EncodeAdam;
+  extern __shared__ __align__(16) uint8_t fsm[];
+  double* b64 = reinterpret_cast<double*>(fsm);       // (j, i) at j*64 + (i ^ (j & 15))
+  float* b32 = reinterpret_cast<float*>(fsm + S * S * 8);  // B[j][i] row-major
+  if (*a.fb_count == 0) return;
+  if (!kEncodeOnly && step_failed(a.status)) return;
+  for (int u = threadIdx.x; u < S * S; u += blockDim.x) {
+    const int j = u >> 6, i = u & 63;
+    b64[j * S + (i ^ (j & 15))] = a.basis.B64[u];
+    b32[u] = a.basis.B[u];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int k = a.geo.k;
+  const bool full_band = k == S;
+  const int dtype = a.geo.dtype;
+  const bool sign_mode = a.geo.sign_mode;
+  const uint64_t nvals = a.geo.nchunks * (uint64_t)k;
+  const unsigned n = *a.fb_count;
+  const unsigned nwarps = gridDim.x * kFixWarps;
+  for (unsigned u = blockIdx.x * kFixWarps + (threadIdx.x >> 5); u < n; u += nwarps) {
+    const uint64_t c = a.fb_list[u];
+    const uint64_t g0 = c * S;
+    const float x0 = a.g[g0 + lane], x1 = a.g[g0 + lane + 32];
+    // exact coefficients
+    double cd0 = 0.0, cd1 = 0.0;
+    const double* r0 = b64 + lane * S;
+    const double* r1 = b64 + (lane + 32) * S;
+    const int sw = lane & 15;
+#pragma unroll 8
+    for (int i = 0; i < S; ++i) {
+      const double xi = (double)__shfl_sync(kFull, i < 32 ? x0 : x1, i & 31);
+      cd0 = __dadd_rn(cd0, __dmul_rn(r0[i ^ sw], xi));
+      cd1 = __dadd_rn(cd1, __dmul_rn(r1[i ^ sw], xi));
+    }
+    // exact TopK: MSB radix select on the |c| bit patterns from their common prefix
+    bool sel0 = true, sel1 = true;
+    if (!full_band) {
+      const uint64_t k0 = (uint64_t)__double_as_longlong(fabs(cd0)), k1 = (uint64_t)__double_as_longlong(fabs(cd1));
+      uint64_t mx = k0 > k1 ? k0 : k1, mn = k0 < k1 ? k0 : k1;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const uint64_t a2 = shfl64(mx, lane ^ o), b2 = shfl64(mn, lane ^ o);
+        mx = a2 > mx ? a2 : mx;
+        mn = b2 < mn ? b2 : mn;
+      }
+      const uint64_t diff = mx ^ mn;
+      const int top = diff ? 63 - __clzll((long long)diff) : -1;
+      uint64_t T = top >= 0 ? (mx & ~((2ull << top) - 1ull)) : mx;
+      bool exact = false;
+      for (int b = top; b >= 0; --b) {
+        const uint64_t cand = T | (1ull << b);
+        const int cnt = __popc(__ballot_sync(kFull, k0 >= cand)) + __popc(__ballot_sync(kFull, k1 >= cand));
+        if (cnt >= k) {
+          T = cand;
+          if (cnt == k) {
+            exact = true;
+            break;
+          }
+        }
+      }
+      if (exact) {
+        sel0 = k0 >= T;
+        sel1 = k1 >= T;
+      } else {  // T is the k-th largest: everything above, then the lowest-index ties
+        const int gt = __popc(__ballot_sync(kFull, k0 > T)) + __popc(__ballot_sync(kFull, k1 > T));
+        const unsigned e0 = __ballot_sync(kFull, k0 == T), e1 = __ballot_sync(kFull, k1 == T);
+        const int need = k - gt;
+        const unsigned lt = lanemask_lt();
+        sel0 = k0 > T || (k0 == T && __popc(e0 & lt) < need);
+        sel1 = k1 > T || (k1 == T && __popc(e0) + __popc(e1 & lt) < need);
+      }
+    }
+    const float c0f = (float)cd0, c1f = (float)cd1;
+    const float w0 = sel0 ? condition_f64(cd0, dtype, sign_mode) : 0.0f;
+    const float w1 = sel1 ? condition_f64(cd1, dtype, sign_mode) : 0.0f;
+    // payload: ascending frequency
+    if (a.body) {
+      const unsigned m0 = __ballot_sync(kFull, sel0), m1 = __ballot_sync(kFull, sel1);
+      const unsigned lt = lanemask_lt();
+      uint32_t* idx = reinterpret_cast<uint32_t*>(a.body);
+      uint8_t* vals = a.body + nvals * 4;
+      if (sel0) {
+        const uint64_t t = c * (uint64_t)k + __popc(m0 & lt);
+        idx[t] = (uint32_t)lane;
+        store_wire_value(vals, t, w0, dtype);
+      }
+      if (sel1) {
+        const uint64_t t = c * (uint64_t)k + __popc(m0) + __popc(m1 & lt);
+        idx[t] = (uint32_t)(lane + 32);
+        store_wire_value(vals, t, w1, dtype);
+      }
+    }
+    if (kEncodeOnly) continue;
+    // D = IDCT(W), W = wire - coef on the selection (k = s: W = wire, D = Q)
+    const float wd0 = full_band ? w0 : (sel0 ? w0 - c0f : 0.0f);
+    const float wd1 = full_band ? w1 : (sel1 ? w1 - c1f : 0.0f);
+    float d0 = 0.0f, d1 = 0.0f;
+    for (int e = 0; e < 2; ++e) {
+      unsigned m = __ballot_sync(kFull, (e ? wd1 : wd0) != 0.0f);
+      while (m) {
+        const int l = __ffs(m) - 1;
+        m &= m - 1;
+        const int j = l + 32 * e;
+        const float wj = __shfl_sync(kFull, e ? wd1 : wd0, l);
+        d0 = fmaf(wj, b32[j * S + lane], d0);
+        d1 = fmaf(wj, b32[j * S + lane + 32], d1);
+      }
+    }
+    const AdamScalars A = a.adam;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const uint64_t gi = g0 + lane + 32 * e;
+      const float d = e ? d1 : d0;
+      const float gp = full_band ? d : (e ? x1 : x0) + d;  // g - local_q + Q (optim.cpp:65)
+      const float m1 = A.beta1 * a.ea_in[gi] + A.one_minus_beta1 * gp;
+      const float m2 = A.beta2 * a.es_in[gi] + A.one_minus_beta2 * gp * gp;
+      float sq;
+      asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(m2 * A.inv_bc2));
+      float pn = a.p_in[gi] - __fdividef(m1 * A.lr_bc1, sq + A.eps);
+      pn -= A.lr_wd * pn;
+      a.ea_out[gi] = m1;
+      a.es_out[gi] = m2;
+      a.p_out[gi] = pn;
+    }
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -940,6 +1097,37 @@ void launch_tc3_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) 
     case ChunkMode::MergeAdam: launch_mode<ChunkMode::MergeAdam>(a, maps, stream); break;
     case ChunkMode::EncodeAdam: launch_mode<ChunkMode::EncodeAdam>(a, maps, stream); break;
     default: break;
+  }
+}
+
+
+void launch_fix64_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) {
+  count_launches(1);
+  auto go = [&](auto kern) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FIX_SMEM);
+      attr = true;
+    }
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFixWarps * 32, FIX_SMEM);
+    kern<<<(unsigned)(sms * (per_sm > 0 ? per_sm : 1)), kFixWarps * 32, FIX_SMEM, stream>>>(a);
+  };
+  const bool sign = a.geo.sign_mode || a.geo.dtype == DMB_TERNARY, f16 = a.geo.dtype == DMB_FP16;
+  switch (mode) {
+    case ChunkMode::StepAdam:
+      if (sign) go(demo_fix64_kernel<ChunkMode::StepAdam, kWireSign>);
+      else if (f16) go(demo_fix64_kernel<ChunkMode::StepAdam, kWireF16>);
+      else go(demo_fix64_kernel<ChunkMode::StepAdam, kWireF32>);
+      break;
+    case ChunkMode::EncodeAdam:
+      if (sign) go(demo_fix64_kernel<ChunkMode::EncodeAdam, kWireSign>);
+      else if (f16) go(demo_fix64_kernel<ChunkMode::EncodeAdam, kWireF16>);
+      else go(demo_fix64_kernel<ChunkMode::EncodeAdam, kWireF32>);
+      break;
+    default: break;  // MergeAdam never defers
   }
 }
 

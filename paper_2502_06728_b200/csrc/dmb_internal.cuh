@@ -161,6 +161,7 @@ struct ChunkArgs {
   const uint32_t* list;
   const unsigned* list_count;
   int force_fp64;
+  uint64_t first_chunk;     // SIMT kernel, non-list mode: start at this chunk (tail fix-up)
   unsigned long long* dbg;  // optional event timestamps (tests / tuning only)
 };
 
@@ -172,6 +173,8 @@ void launch_tc_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream);
 bool tc_enabled();
 bool tc3_supported(ChunkMode mode, const ChunkArgs& a);
 void launch_tc3_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream);
+// exact FP64 re-derivation of the full chunks listed in a.fb_list / a.fb_count
+void launch_fix64_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream);
 
 // Elementwise (Full / DiLoCo / Striding / Random) paths.
 struct SparseSel {
