@@ -198,6 +198,11 @@ int dmb_status(dmb_ctx* ctx, void* stream, int64_t* first_bad);
 int dmb_fallback_chunks(dmb_ctx* ctx, void* stream, uint64_t* count);
 /* kernels launched by this context since creation (host counter) */
 uint64_t dmb_launch_count(dmb_ctx* ctx);
+/* instrumentation: when enabled, CUDA events bracket every launch of the dominant
+ * tensor-core step kernel on its stream; read returns their summed time and count
+ * (synchronizing on the recorded events) and clears them */
+int dmb_kernel_timer_enable(int on);
+int dmb_kernel_timer_read(double* total_ms, uint64_t* launches);
 
 #ifdef __cplusplus
 }

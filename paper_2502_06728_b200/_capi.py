@@ -97,6 +97,8 @@ _SIGS = {
     "dmb_status": (C.c_int, [P, P, C.POINTER(C.c_int64)]),
     "dmb_fallback_chunks": (C.c_int, [P, P, PU64]),
     "dmb_launch_count": (U64, [P]),
+    "dmb_kernel_timer_enable": (C.c_int, [C.c_int]),
+    "dmb_kernel_timer_read": (C.c_int, [C.POINTER(C.c_double), PU64]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -7,6 +7,9 @@
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
+#include <mutex>
+#include <tuple>
+#include <vector>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -18,6 +21,35 @@
 namespace dmb {
 static std::atomic<uint64_t> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+namespace {
+std::mutex g_timer_mu;
+bool g_timer_on = false;
+std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_timer_pairs;  // recorded, not yet read
+std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_timer_pool;   // read, reusable
+cudaEvent_t g_timer_open = nullptr;
+}  // namespace
+void timer_begin(cudaStream_t stream) {
+  std::lock_guard<std::mutex> l(g_timer_mu);
+  if (!g_timer_on) return;
+  cudaEvent_t b = nullptr, e = nullptr;
+  if (!g_timer_pool.empty()) {
+    std::tie(b, e) = g_timer_pool.back();
+    g_timer_pool.pop_back();
+  } else {
+    cudaEventCreate(&b);
+    cudaEventCreate(&e);
+  }
+  cudaEventRecord(b, stream);
+  g_timer_pairs.emplace_back(b, e);
+  g_timer_open = e;
+}
+void timer_end(cudaStream_t stream) {
+  std::lock_guard<std::mutex> l(g_timer_mu);
+  if (!g_timer_on || !g_timer_open) return;
+  cudaEventRecord(g_timer_open, stream);
+  g_timer_open = nullptr;
+}
 }  // namespace dmb
 
 using namespace dmb;
@@ -884,6 +916,30 @@ int dmb_fallback_chunks(dmb_ctx* ctx, void* stream, uint64_t* count) {
 
 // tuning hook (not in the public header): device buffer of 32 x 16 u64 timestamps
 void dmb_debug_events(unsigned long long* d_buf) { g_dbg = d_buf; }
+
+int dmb_kernel_timer_enable(int on) {
+  std::lock_guard<std::mutex> l(g_timer_mu);
+  g_timer_on = on != 0;
+  return DMB_OK;
+}
+
+int dmb_kernel_timer_read(double* total_ms, uint64_t* launches) {
+  std::lock_guard<std::mutex> l(g_timer_mu);
+  double t = 0.0;
+  uint64_t n = 0;
+  for (auto& pr : g_timer_pairs) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(pr.second) == cudaSuccess && cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) {
+      t += ms;
+      ++n;
+    }
+    g_timer_pool.push_back(pr);
+  }
+  g_timer_pairs.clear();
+  if (total_ms) *total_ms = t;
+  if (launches) *launches = n;
+  return DMB_OK;
+}
 
 uint64_t dmb_launch_count(dmb_ctx* ctx) {
   (void)ctx;

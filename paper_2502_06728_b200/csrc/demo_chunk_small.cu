@@ -17,7 +17,9 @@ void launch_chunk_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream
     // re-derived exactly by the FP64 fix-up kernel; a partial last chunk (its own
     // length and basis) goes through the SIMT kernel
     cudaMemsetAsync(a.fb_count, 0, sizeof(unsigned), stream);
+    timer_begin(stream);
     launch_tc3_kernel(mode, a, stream);
+    timer_end(stream);
     launch_fix64_kernel(mode, a, stream);
     if (a.geo.len % a.geo.s) {
       ChunkArgs tail = a;
@@ -28,7 +30,9 @@ void launch_chunk_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream
   }
   if (tc_enabled() && a.fb_list && a.fb_count && tc_supported(mode, a)) {
     cudaMemsetAsync(a.fb_count, 0, sizeof(unsigned), stream);
+    timer_begin(stream);
     launch_tc_kernel(mode, a, stream);
+    timer_end(stream);
     ChunkArgs fix = a;
     fix.list = a.fb_list;
     fix.list_count = a.fb_count;

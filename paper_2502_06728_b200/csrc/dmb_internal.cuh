@@ -12,6 +12,9 @@ namespace dmb {
 
 // kernels launched through this library (the bench's gpu_launches evidence)
 void count_launches(int n);
+// dmb_kernel_timer_*: events around the dominant tensor-core kernel's launches
+void timer_begin(cudaStream_t stream);
+void timer_end(cudaStream_t stream);
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr unsigned long long kNoBad = ~0ull;
