@@ -11,7 +11,15 @@ bool tc_enabled() {
   return !(e && e[0] == '0');
 }
 
-void launch_chunk_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) {
+// DMB_FORCE_FP64=1 (tests): every chunk takes the exact FP64 re-derivation path
+static bool force_fp64_env() {
+  const char* e = std::getenv("DMB_FORCE_FP64");
+  return e && e[0] == '1';
+}
+
+void launch_chunk_kernel(ChunkMode mode, const ChunkArgs& a_in, cudaStream_t stream) {
+  ChunkArgs a = a_in;
+  if (force_fp64_env()) a.force_fp64 = 1;
   if (tc_enabled() && a.fb_list && a.fb_count && tc3_supported(mode, a)) {
     // warp-specialised tensor-core kernel; the chunks its FP32 bound cannot certify are
     // re-derived exactly by the FP64 fix-up kernel; a partial last chunk (its own

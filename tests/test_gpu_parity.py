@@ -439,9 +439,10 @@ def test_tc_and_simt_paths_agree(oracle, monkeypatch, k):
         chunk_close(host(enc.local_q), want["local_q"], 64, what=f"local_q tc={flag}")
 
 
-@pytest.mark.parametrize("opt_kind", ["sgd", "adamw"])
-def test_tc_fused_step_matches_oracle(oracle, monkeypatch, opt_kind):
-    """dmb_step_*_local through the tensor-core kernel vs the oracle's prepare/merge/apply"""
+@pytest.mark.parametrize("opt_kind,force", [("sgd", False), ("adamw", False), ("sgd", True), ("adamw", True)])
+def test_tc_fused_step_matches_oracle(oracle, monkeypatch, opt_kind, force):
+    """dmb_step_*_local through the tensor-core kernel vs the oracle's prepare/merge/apply;
+    force: every chunk is deferred to the exact FP64 fix-up (DMB_FORCE_FP64=1)"""
     import ctypes as C
 
     from paper_2502_06728_b200 import _capi
@@ -449,6 +450,8 @@ def test_tc_fused_step_matches_oracle(oracle, monkeypatch, opt_kind):
 
     p = P()
     monkeypatch.setenv("DMB_TC", "1")
+    if force:
+        monkeypatch.setenv("DMB_FORCE_FP64", "1")
     n = 64 * 128 * 12 + 100
     rng = np.random.default_rng(5)
     g = (rng.standard_normal(n) * 1e-3).astype(np.float32)
@@ -495,3 +498,64 @@ def test_tc_fused_step_matches_oracle(oracle, monkeypatch, opt_kind):
         update_close(host(pd), pw, p0, lr, 64)
     idx = body[: 4 * want["freq_indices"].size].view(torch.int32).cpu().numpy().astype(np.uint32)
     assert np.array_equal(idx, want["freq_indices"])
+
+
+@pytest.mark.parametrize("k,force", [(32, False), (8, False), (32, True)])
+def test_tc_cluster_adamw_prepare_merge_matches_oracle(oracle, monkeypatch, k, force):
+    """The N>1 path as cluster.py drives it: dmb_adamw_prepare (no local_q: the tensor-core
+    encode kernel) on R members' gradients, then dmb_merge_apply_adamw of the R bodies for one
+    member (the tensor-core merge kernel) -- payloads and state against the oracle's
+    select_and_encode / decode_and_merge / adamw_apply (cluster.cpp:193-231)."""
+    import ctypes as C
+
+    from paper_2502_06728_b200 import _capi
+    from paper_2502_06728_b200.core import _ptr, _stream, context
+
+    p = P()
+    monkeypatch.setenv("DMB_TC", "1")
+    if force:
+        monkeypatch.setenv("DMB_FORCE_FP64", "1")
+    lib = _capi.lib
+    n = 64 * 128 * 6 + 64 * 3 + 7  # partial last tile and chunk
+    R, own, step, lr = 3, 1, 5, 0.002
+    rng = np.random.default_rng(31 + k)
+    gs = [(rng.standard_normal(n) * 1e-3).astype(np.float32) for _ in range(R)]
+    rep = Rep(scheme=DEMO, chunk_size=64, top_k=k, compression=k / 64, sign_mode=True, seed=1234)
+    c = rep_to_cfg(rep).c()
+    cap = int(lib.dmb_update_capacity(C.byref(c), n))
+    ups = (_capi.Update * R)()
+    keep = []
+    wants = []
+    for r in range(R):
+        gd = dev(gs[r])
+        body = torch.zeros(cap, dtype=torch.uint8, device="cuda")
+        hdr = _capi.Update()
+        hdr.body = body.data_ptr()
+        rc = lib.dmb_adamw_prepare(context().h, _ptr(gd), n, C.byref(c), step, 0, C.byref(hdr), None, _stream())
+        assert rc == 0, lib.dmb_last_error()
+        p.status()
+        want = oracle.select_and_encode(gs[r].astype(np.float64), rep, step, 0)
+        wants.append(want)
+        ni = want["freq_indices"].size
+        idx = body[: 4 * ni].view(torch.int32).cpu().numpy().astype(np.uint32)
+        assert np.array_equal(idx, want["freq_indices"]), f"member {r} indices"
+        vals = body[4 * ni: 8 * ni].view(torch.float32).cpu().numpy()
+        assert np.array_equal(vals, want["values"].astype(np.float32)), f"member {r} values"
+        ups[r] = hdr
+        keep += [gd, body]
+    p0 = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    ea0 = (rng.standard_normal(n) * 0.05).astype(np.float32)
+    es0 = (ea0.astype(np.float64) ** 2 * 4 + 1e-4).astype(np.float32)
+    pd, ead, esd, god = dev(p0), dev(ea0), dev(es0), dev(gs[own])
+    o = p.OptimizerConfig(p.OptimizerKind.DecoupledAdamW).c()
+    steps = C.c_uint64(4)
+    rc = lib.dmb_merge_apply_adamw(context().h, ups, R, own, C.byref(c), _ptr(pd), _ptr(ead), _ptr(esd),
+                                   C.byref(steps), _ptr(god), n, step, C.byref(o), lr, _stream())
+    assert rc == 0, lib.dmb_last_error()
+    p.status()
+    q = oracle.decode_and_merge(rep, [w["values"] for w in wants], [w["freq_indices"] for w in wants], n, step, 0)
+    pw, ew, sw = p0.astype(np.float64), ea0.astype(np.float64), es0.astype(np.float64)
+    oracle.adamw_apply(pw, ew, sw, 4, gs[own].astype(np.float64), wants[own]["local_q"], q, 0.9, 0.999, 1e-8, 0.0, lr)
+    chunk_close(host(ead), ew, 64, tol=1e-4, what="exp_avg")
+    chunk_close(host(esd), sw, 64, tol=1e-4, what="exp_avg_sq")
+    update_close(host(pd), pw, p0, lr, 64)
