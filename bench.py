@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--sign", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--buckets", type=int, default=8,
+                    help="N>1: chunk-aligned buckets of the shard pipelined through prepare / all-gather / merge")
+    ap.add_argument("--sm-reserve", type=int, default=32,
+                    help="N>1: SMs the step kernels leave free for the concurrent NCCL all-gather")
     ap.add_argument("--cpu-sample", type=int, default=1 << 22, help="elements per CPU thread")
     ap.add_argument("--layout", default=None, help="SxR (shards x replicas) for N>1; default 1xN")
     return ap.parse_args()
@@ -228,7 +232,8 @@ def run_ours(args, rank, world, local_rank):
         assert S * R == world, f"layout {S}x{R} does not match {world} ranks"
         topo = Topology(nodes=R, accels_per_node=S)
         sg, rg = groups_for(topo, rank)
-        cluster = HybridCluster(topo, L, opt, cfg, params, rank, sg, rg)
+        os.environ["DMB_SM_RESERVE"] = str(args.sm_reserve)
+        cluster = HybridCluster(topo, L, opt, cfg, params, rank, sg, rg, buckets=args.buckets)
         del params
 
     def check(rc):

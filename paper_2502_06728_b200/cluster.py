@@ -124,7 +124,8 @@ class HybridCluster:
     """
 
     def __init__(self, topo: Topology, param_count: int, opt: OptimizerConfig, rep: ReplicatorConfig,
-                 initial_params: torch.Tensor, rank: int, shard_group=None, replica_group=None):
+                 initial_params: torch.Tensor, rank: int, shard_group=None, replica_group=None,
+                 buckets: int = 8):
         self.topo, self.opt, self.rep = topo, opt, rep
         self.rank = rank
         self.node, self.accel = divmod(rank, topo.accels_per_node)
@@ -146,12 +147,74 @@ class HybridCluster:
         self.exchange = ReplicaExchange(replica_group, topo.nodes, self.capacity, self.device)
         self.shard_grad = torch.empty(self.spec.extent, dtype=torch.float32, device=self.device)
         self.ledger: List[StepTraffic] = []
+        # Bucketed exchange (DeMo, R > 1): chunk-aligned slices of the shard, each prepared,
+        # all-gathered and merged on its own, so the NVLink transfer of bucket b overlaps the
+        # prepare of b+1 and the merge of b-1.  DeMo's selection is chunk-local, so every
+        # bucket's payload is the reference's body of that sub-vector and the merged result
+        # is the unbucketed one (Random / Striding / DiLoCo / Full use one bucket).
+        self.buckets = []
+        if rep.scheme == Scheme.DeMo and topo.nodes > 1 and buckets > 1 and L > 0:
+            tile = 128 * rep.chunk_size
+            edges = sorted({min(L, (L * b // buckets) // tile * tile) for b in range(buckets)} | {L})
+            for lo, hi in zip(edges[:-1], edges[1:]):
+                cap = int(lib.dmb_update_capacity(C.byref(c), hi - lo))
+                self.buckets.append(dict(lo=lo, hi=hi, cap=cap,
+                                         own=torch.empty(cap, dtype=torch.uint8, device=self.device),
+                                         gathered=torch.empty(topo.nodes * cap, dtype=torch.uint8,
+                                                              device=self.device)))
 
     def _reduce_scatter(self, grad_full: torch.Tensor) -> torch.Tensor:
         A = self.topo.accels_per_node
         if A == 1:
             return grad_full[: self.spec.extent]
         return reduce_scatter_mean(self.shard_grad, grad_full, A, self.shard_group)
+
+    def _step_bucketed(self, step: int, lr: float, g_shard: torch.Tensor, tr: StepTraffic) -> None:
+        R = self.topo.nodes
+        ctx = context(self.device).h
+        c, o = self.rep.c(), self.opt.c()
+        st = _stream(g_shard)
+        sgd = self.opt.kind == OptimizerKind.DemoSgd
+        pending = []
+
+        def merge(b, hdr, work):
+            work.wait()  # the compute stream waits for the gather; the host does not
+            lo, hi = b["lo"], b["hi"]
+            ups = (_capi.Update * R)()
+            for r in range(R):
+                ups[r] = hdr
+                ups[r].body = b["gathered"][r * b["cap"]:].data_ptr()
+            if sgd:
+                _check(lib.dmb_merge_apply_sgd(ctx, ups, R, C.byref(c), _ptr(self.params[lo:hi]),
+                                               _ptr(g_shard[lo:hi]), hi - lo, step, float(lr), st))
+            else:
+                _check(lib.dmb_merge_apply_adamw(ctx, ups, R, self.node, C.byref(c), _ptr(self.params[lo:hi]),
+                                                 _ptr(self.exp_avg[lo:hi]), _ptr(self.exp_avg_sq[lo:hi]),
+                                                 C.byref(self.steps_b), _ptr(g_shard[lo:hi]), hi - lo, step,
+                                                 C.byref(o), float(lr), st))
+
+        steps0 = self.steps.value
+        for b in self.buckets:
+            lo, hi = b["lo"], b["hi"]
+            hdr = _capi.Update()
+            hdr.body = b["own"].data_ptr()
+            if sgd:
+                _check(lib.dmb_demo_sgd_prepare(ctx, _ptr(g_shard[lo:hi]), _ptr(self.m[lo:hi]), _ptr(self.m[lo:hi]),
+                                                hi - lo, C.byref(o), C.byref(c), step, self.accel, C.byref(hdr),
+                                                None, None, st))
+            else:
+                _check(lib.dmb_adamw_prepare(ctx, _ptr(g_shard[lo:hi]), hi - lo, C.byref(c), step, self.accel,
+                                             C.byref(hdr), None, st))
+            tr.inter_bytes += int(hdr.bytes) * (R - 1)
+            work = dist.all_gather_into_tensor(b["gathered"], b["own"][: b["cap"]], group=self.replica_group,
+                                               async_op=True)
+            if pending:
+                self.steps_b = C.c_uint64(steps0)
+                merge(*pending.pop())
+            pending.append((b, hdr, work))
+        self.steps_b = C.c_uint64(steps0)
+        merge(*pending.pop())
+        self.steps = self.steps_b  # every bucket advanced the AdamW counter from the same value
 
     def step(self, step: int, lr: float, grad_full: torch.Tensor, check: bool = True) -> StepTraffic:
         topo = self.topo
@@ -161,6 +224,13 @@ class HybridCluster:
         A = topo.accels_per_node
         tr.intra_bytes = A * (A - 1) * self.spec.extent * 4  # ring model, cluster.cpp:87
         tr.reduce_scatter_events = 1
+        if self.buckets:
+            tr.synchronize_events = 1
+            self._step_bucketed(step, lr, g_shard, tr)
+            if check:
+                status(self.device)
+            self.ledger.append(tr)
+            return tr
         ctx = context(self.device).h
         st = _stream(g_shard)
         c, o = self.rep.c(), self.opt.c()
