@@ -51,7 +51,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--buckets", type=int, default=8,
                     help="N>1: chunk-aligned buckets of the shard pipelined through prepare / all-gather / merge")
-    ap.add_argument("--sm-reserve", type=int, default=32,
+    ap.add_argument("--wire", choices=["mask", "reference"], default="mask",
+                    help="N>1 DeMo exchange layout: lossless u64-mask + packed values, or the reference body")
+    ap.add_argument("--sm-reserve", type=int, default=0,
                     help="N>1: SMs the step kernels leave free for the concurrent NCCL all-gather")
     ap.add_argument("--cpu-sample", type=int, default=1 << 22, help="elements per CPU thread")
     ap.add_argument("--layout", default=None, help="SxR (shards x replicas) for N>1; default 1xN")
@@ -233,7 +235,7 @@ def run_ours(args, rank, world, local_rank):
         topo = Topology(nodes=R, accels_per_node=S)
         sg, rg = groups_for(topo, rank)
         os.environ["DMB_SM_RESERVE"] = str(args.sm_reserve)
-        cluster = HybridCluster(topo, L, opt, cfg, params, rank, sg, rg, buckets=args.buckets)
+        cluster = HybridCluster(topo, L, opt, cfg, params, rank, sg, rg, buckets=args.buckets, wire=args.wire)
         del params
 
     def check(rc):
@@ -302,7 +304,7 @@ def run_ours(args, rank, world, local_rank):
     B_alg = 28 if args.optimizer == "adamw" else 20  # bytes per param, SURVEY 8(d)
     if distributed:
         # prepare reads g (4); merge+apply reads g again + p/m/v r/w (28) + (1+R) payloads
-        P_b = (args.topk / args.chunk) * 8
+        P_b = cluster.payload_bytes_per_param  # the exchanged body per parameter (MASK or reference)
         B_alg = (32 if args.optimizer == "adamw" else 24) + (1 + cluster.topo.nodes) * P_b
     step_ms = statistics.median(per_step)
     # dominant kernel: its own launches, timed by events on its stream inside the timed

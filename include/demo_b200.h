@@ -60,6 +60,12 @@ enum { DMB_DEMO = 1, DMB_RANDOM = 2, DMB_STRIDING = 3, DMB_DILOCO = 4, DMB_FULL 
 enum { DMB_FP32 = 0, DMB_FP16 = 1, DMB_TERNARY = 2 };
 /* optim.hpp:11 */
 enum { DMB_DEMO_SGD = 0, DMB_DECOUPLED_ADAMW = 1 };
+/* DeMo body layout.  REFERENCE: replicate.cpp:316-356 (u32 indices, then values per dtype).
+ * MASK (exchange-only, lossless): one u64 frequency mask per chunk (bit j = frequency j),
+ * then the values in ascending frequency per chunk -- as 2-bit codes when sign_mode or
+ * ternary (the values are exactly -1/0/+1), else per dtype.  At s=64, k=32, sign on the
+ * body is 16 B per chunk instead of 256 B.  dmb_serialize always emits the reference bytes. */
+enum { DMB_WIRE_REFERENCE = 0, DMB_WIRE_MASK = 1, DMB_WIRE_MASK_SIGN = 2 /* MASK, 2-bit values */ };
 
 /* ReplicatorConfig, replicate.hpp:28-39 */
 typedef struct {
@@ -91,7 +97,7 @@ typedef struct {
   int32_t empty;
   uint64_t step;
   uint32_t shard_id;
-  uint32_t _pad;
+  uint32_t wire_format;  /* DMB_WIRE_REFERENCE, or DMB_WIRE_MASK (set by the encoder) */
   uint64_t length;
   uint64_t chunk_size;
   uint64_t top_k;
@@ -198,6 +204,13 @@ int dmb_status(dmb_ctx* ctx, void* stream, int64_t* first_bad);
 int dmb_fallback_chunks(dmb_ctx* ctx, void* stream, uint64_t* count);
 /* kernels launched by this context since creation (host counter) */
 uint64_t dmb_launch_count(dmb_ctx* ctx);
+/* DeMo exchange format of the updates this context encodes (DMB_WIRE_REFERENCE default;
+ * DMB_WIRE_MASK selects MASK, recorded as DMB_WIRE_MASK_SIGN in updates whose values are
+ * signs).
+ * DMB_WIRE_MASK applies where the tensor-core AdamW path runs (s = 64, whole chunks, no
+ * local_q output); elsewhere the encoder keeps the reference layout.  Merges read each
+ * update's wire_format. */
+int dmb_set_wire_format(dmb_ctx* ctx, int32_t format);
 /* instrumentation: when enabled, CUDA events bracket every launch of the dominant
  * tensor-core step kernel on its stream; read returns their summed time and count
  * (synchronizing on the recorded events) and clears them */

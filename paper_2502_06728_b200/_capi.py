@@ -47,7 +47,7 @@ class Update(C.Structure):
         ("empty", C.c_int32),
         ("step", C.c_uint64),
         ("shard_id", C.c_uint32),
-        ("_pad", C.c_uint32),
+        ("wire_format", C.c_uint32),
         ("length", C.c_uint64),
         ("chunk_size", C.c_uint64),
         ("top_k", C.c_uint64),
@@ -97,6 +97,7 @@ _SIGS = {
     "dmb_status": (C.c_int, [P, P, C.POINTER(C.c_int64)]),
     "dmb_fallback_chunks": (C.c_int, [P, P, PU64]),
     "dmb_launch_count": (U64, [P]),
+    "dmb_set_wire_format": (C.c_int, [P, C.c_int32]),
     "dmb_kernel_timer_enable": (C.c_int, [C.c_int]),
     "dmb_kernel_timer_read": (C.c_int, [C.POINTER(C.c_double), PU64]),
 }

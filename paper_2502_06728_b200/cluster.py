@@ -26,7 +26,8 @@ import torch
 import torch.distributed as dist
 
 from . import _capi
-from .core import (OptimizerConfig, OptimizerKind, ReplicatorConfig, Scheme, _check, _ptr, _stream,
+from .core import (OptimizerConfig, OptimizerKind, ReplicatorConfig, Scheme, TransferDtype, _check, _ptr,
+                   _stream,
                    context, status)
 from ._capi import lib
 
@@ -67,6 +68,7 @@ class StepTraffic:
     inter_bytes: int = 0
     reduce_scatter_events: int = 0
     synchronize_events: int = 0
+    inter_bytes_reference: int = 0  # the reference wire format's bytes for the same exchange
 
 
 def groups_for(topo: Topology, rank: int, backend: Optional[str] = None):
@@ -125,7 +127,7 @@ class HybridCluster:
 
     def __init__(self, topo: Topology, param_count: int, opt: OptimizerConfig, rep: ReplicatorConfig,
                  initial_params: torch.Tensor, rank: int, shard_group=None, replica_group=None,
-                 buckets: int = 8):
+                 buckets: int = 8, wire: str = "mask"):
         self.topo, self.opt, self.rep = topo, opt, rep
         self.rank = rank
         self.node, self.accel = divmod(rank, topo.accels_per_node)
@@ -152,16 +154,25 @@ class HybridCluster:
         # prepare of b+1 and the merge of b-1.  DeMo's selection is chunk-local, so every
         # bucket's payload is the reference's body of that sub-vector and the merged result
         # is the unbucketed one (Random / Striding / DiLoCo / Full use one bucket).
+        # MASK exchange layout (include/demo_b200.h): u64 frequency mask per chunk + values,
+        # lossless, used where the tensor-core AdamW kernels run (s = 64, whole chunks)
+        self.mask_wire = (wire == "mask" and rep.scheme == Scheme.DeMo and opt.kind == OptimizerKind.DecoupledAdamW
+                          and rep.chunk_size == 64 and L % 64 == 0)
         self.buckets = []
         if rep.scheme == Scheme.DeMo and topo.nodes > 1 and buckets > 1 and L > 0:
             tile = 128 * rep.chunk_size
             edges = sorted({min(L, (L * b // buckets) // tile * tile) for b in range(buckets)} | {L})
+            vbits = 2 if (rep.sign_mode or rep.transfer_dtype == TransferDtype.Ternary) else \
+                (16 if rep.transfer_dtype == TransferDtype.Fp16 else 32)
             for lo, hi in zip(edges[:-1], edges[1:]):
                 cap = int(lib.dmb_update_capacity(C.byref(c), hi - lo))
-                self.buckets.append(dict(lo=lo, hi=hi, cap=cap,
+                nch = (hi - lo) // 64
+                xfer = cap if not self.mask_wire else ((8 * nch + (nch * rep.top_k * vbits + 7) // 8 + 15) // 16) * 16
+                self.buckets.append(dict(lo=lo, hi=hi, cap=cap, xfer=xfer,
                                          own=torch.empty(cap, dtype=torch.uint8, device=self.device),
-                                         gathered=torch.empty(topo.nodes * cap, dtype=torch.uint8,
+                                         gathered=torch.empty(topo.nodes * xfer, dtype=torch.uint8,
                                                               device=self.device)))
+            self.payload_bytes_per_param = sum(b["xfer"] for b in self.buckets) / L
 
     def _reduce_scatter(self, grad_full: torch.Tensor) -> torch.Tensor:
         A = self.topo.accels_per_node
@@ -183,7 +194,7 @@ class HybridCluster:
             ups = (_capi.Update * R)()
             for r in range(R):
                 ups[r] = hdr
-                ups[r].body = b["gathered"][r * b["cap"]:].data_ptr()
+                ups[r].body = b["gathered"][r * b["xfer"]:].data_ptr()
             if sgd:
                 _check(lib.dmb_merge_apply_sgd(ctx, ups, R, C.byref(c), _ptr(self.params[lo:hi]),
                                                _ptr(g_shard[lo:hi]), hi - lo, step, float(lr), st))
@@ -194,6 +205,15 @@ class HybridCluster:
                                                  C.byref(o), float(lr), st))
 
         steps0 = self.steps.value
+        if self.mask_wire:
+            _check(lib.dmb_set_wire_format(ctx, 1))
+        try:
+            self._pipeline(step, lr, g_shard, tr, merge, pending, steps0, ctx, c, o, st, sgd, R)
+        finally:
+            if self.mask_wire:
+                lib.dmb_set_wire_format(ctx, 0)
+
+    def _pipeline(self, step, lr, g_shard, tr, merge, pending, steps0, ctx, c, o, st, sgd, R):
         for b in self.buckets:
             lo, hi = b["lo"], b["hi"]
             hdr = _capi.Update()
@@ -206,7 +226,9 @@ class HybridCluster:
                 _check(lib.dmb_adamw_prepare(ctx, _ptr(g_shard[lo:hi]), hi - lo, C.byref(c), step, self.accel,
                                              C.byref(hdr), None, st))
             tr.inter_bytes += int(hdr.bytes) * (R - 1)
-            work = dist.all_gather_into_tensor(b["gathered"], b["own"][: b["cap"]], group=self.replica_group,
+            tr.inter_bytes_reference += int(lib.dmb_wire_bytes(hdr.n_values, hdr.n_indices,
+                                                                self.rep.transfer_dtype)) * (R - 1)
+            work = dist.all_gather_into_tensor(b["gathered"], b["own"][: b["xfer"]], group=self.replica_group,
                                                async_op=True)
             if pending:
                 self.steps_b = C.c_uint64(steps0)

@@ -137,6 +137,7 @@ struct dmb_ctx {
   uint32_t* fb_list = nullptr;  // chunks the tensor-core path hands to the FP64 kernel
   unsigned* fb_count = nullptr;
   uint64_t fb_cap = 0;
+  int wire_format = DMB_WIRE_REFERENCE;  // DeMo exchange layout of the updates encoded here
 };
 
 namespace {
@@ -295,11 +296,33 @@ uint64_t capacity(const dmb_rep_cfg* cfg, uint64_t len) {
   return ((wire_bytes(nv, ni, cfg->transfer_dtype) + 15) / 16) * 16 + 16;
 }
 
+float half_to_float(uint16_t h) {
+  __half_raw r;
+  r.x = h;
+  return __half2float(__half(r));
+}
+uint16_t float_to_half(float v) {
+  const __half_raw r = __float2half_rn(v);
+  return r.x;
+}
+
+bool is_mask(const dmb_update* u) { return u->scheme == DMB_DEMO && u->wire_format != DMB_WIRE_REFERENCE; }
+uint64_t chunks_of(const dmb_update* u) { return u->chunk_size ? (u->length + u->chunk_size - 1) / u->chunk_size : 0; }
+// dtype of the packed values actually in the body
+int32_t body_value_dtype(const dmb_update* u, int32_t dtype) {
+  return u->wire_format == DMB_WIRE_MASK_SIGN ? DMB_TERNARY : dtype;
+}
+uint64_t mask_body_bytes(const dmb_update* u, int32_t dtype) {
+  return 8 * chunks_of(u) + (u->n_values * value_bits(body_value_dtype(u, dtype)) + 7) / 8;
+}
+
 uint8_t* values_region(const dmb_update* u) {
+  if (is_mask(u)) return static_cast<uint8_t*>(u->body) + 8 * chunks_of(u);
   return static_cast<uint8_t*>(u->body) + u->n_indices * 4;
 }
 
 int prep_values_region(const dmb_update* u, int32_t dtype, cudaStream_t st) {
+  dtype = body_value_dtype(u, dtype);
   if (dtype == DMB_TERNARY && u->n_values) {
     const uint64_t vb = (u->n_values * 2 + 7) / 8;
     DMB_CUDA_TRY(cudaMemsetAsync(values_region(u), 0, ((vb + 3) / 4) * 4, st));
@@ -435,6 +458,9 @@ int validate_updates(const dmb_update* ups, uint64_t n, const dmb_rep_cfg* cfg) 
     case DMB_DEMO: {
       if (r.chunk_size != cfg->chunk_size || r.top_k != cfg->top_k)
         return fail(DMB_PROTOCOL, "chunk geometry does not match the config");
+      for (uint64_t i = 0; i < n; ++i)
+        if (ups[i].wire_format != r.wire_format)
+          return fail(DMB_PROTOCOL, "updates of one merge use different wire formats");
       const uint64_t expected = ((r.length + cfg->chunk_size - 1) / cfg->chunk_size) * cfg->top_k;
       for (uint64_t i = 0; i < n; ++i)
         if (ups[i].n_indices != expected || ups[i].n_values != expected)
@@ -478,7 +504,6 @@ int encode(dmb_ctx* ctx, DevStatus* st, bool sgd, const float* g, const float* m
   if (!out->body && out->n_values) return fail(DMB_CONFIG, "update body is NULL");
   if (len == 0) return DMB_OK;
   if (cfg->scheme == DMB_DEMO) {
-    if (int rc = prep_values_region(out, cfg->transfer_dtype, s)) return rc;
     ChunkArgs a{};
     a.geo = geometry(cfg, len);
     if (int rc = get_basis(ctx, a.geo.s, &a.basis)) return rc;
@@ -491,6 +516,13 @@ int encode(dmb_ctx* ctx, DevStatus* st, bool sgd, const float* g, const float* m
     a.sgd = sgd_scalars(beta, 0.0);
     a.status = st;
     if (int rc = attach_fallback(ctx, &a)) return rc;
+    if (ctx->wire_format != DMB_WIRE_REFERENCE && !sgd && len % cfg->chunk_size == 0 && tc_enabled() &&
+        tc3_supported(ChunkMode::EncodeAdam, a)) {
+      out->wire_format = (cfg->sign_mode || cfg->transfer_dtype == DMB_TERNARY) ? DMB_WIRE_MASK_SIGN : DMB_WIRE_MASK;
+      out->bytes = mask_body_bytes(out, cfg->transfer_dtype);
+      a.geo.wire_mask = 1;
+    }
+    if (int rc = prep_values_region(out, cfg->transfer_dtype, s)) return rc;
     launch_chunk_kernel(sgd ? ChunkMode::EncodeSgd : ChunkMode::EncodeAdam, a, s);
     return last_launch();
   }
@@ -628,6 +660,43 @@ int dmb_serialize(const dmb_update* u, int32_t dtype, uint8_t* host_out, uint64_
   if (cap < 9 + body) return fail(DMB_CONFIG, "serialize: buffer too small");
   host_out[0] = (uint8_t)u->scheme;
   for (int i = 0; i < 8; ++i) host_out[1 + i] = (uint8_t)(u->n_values >> (8 * i));
+  if (body && is_mask(u)) {  // expand the exchange layout into the reference body
+    std::vector<uint8_t> m(mask_body_bytes(u, dtype));
+    DMB_CUDA_TRY(cudaMemcpyAsync(m.data(), u->body, m.size(), cudaMemcpyDeviceToHost, as_stream(stream)));
+    DMB_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+    const uint64_t nc = chunks_of(u), k = u->top_k;
+    const uint8_t* vin = m.data() + 8 * nc;
+    const int32_t vd = body_value_dtype(u, dtype);
+    uint8_t* idx = host_out + 9;
+    uint8_t* vout = idx + u->n_indices * 4;
+    if (dtype == DMB_TERNARY) std::memset(vout, 0, (u->n_values * 2 + 7) / 8);
+    for (uint64_t c = 0; c < nc; ++c) {
+      uint64_t mk;
+      std::memcpy(&mk, m.data() + 8 * c, 8);
+      uint64_t t = c * k;
+      for (uint32_t j = 0; j < 64 && mk; ++j, mk >>= 1) {
+        if (!(mk & 1)) continue;
+        std::memcpy(idx + 4 * t, &j, 4);
+        float v;
+        if (vd == DMB_TERNARY) {
+          const uint32_t code = (vin[t >> 2] >> (2 * (t & 3))) & 3u;
+          v = code == 1u ? 1.0f : (code == 2u ? -1.0f : 0.0f);
+        } else if (vd == DMB_FP16) {
+          uint16_t h;
+          std::memcpy(&h, vin + 2 * t, 2);
+          v = half_to_float(h);
+        } else {
+          std::memcpy(&v, vin + 4 * t, 4);
+        }
+        if (dtype == DMB_FP32) std::memcpy(vout + 4 * t, &v, 4);
+        else if (dtype == DMB_FP16) { const uint16_t h = float_to_half(v); std::memcpy(vout + 2 * t, &h, 2); }
+        else { const uint32_t code = v > 0.0f ? 1u : (v < 0.0f ? 2u : 0u); vout[t >> 2] |= (uint8_t)(code << (2 * (t & 3))); }
+        ++t;
+      }
+    }
+    *written = 9 + body;
+    return DMB_OK;
+  }
   if (body) {
     DMB_CUDA_TRY(cudaMemcpyAsync(host_out + 9, u->body, body, cudaMemcpyDeviceToHost, as_stream(stream)));
     DMB_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
@@ -669,7 +738,7 @@ int dmb_deserialize(const uint8_t* buf, uint64_t size, int32_t dtype, const dmb_
 
 int dmb_update_values(const dmb_update* u, int32_t dtype, float* d_values, void* stream) {
   if (u->n_values == 0) return DMB_OK;
-  launch_unpack_values(values_region(u), u->n_values, dtype, d_values, as_stream(stream));
+  launch_unpack_values(values_region(u), u->n_values, body_value_dtype(u, dtype), d_values, as_stream(stream));
   return last_launch();
 }
 
@@ -793,6 +862,11 @@ int dmb_merge_apply_adamw(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_up
     a.adam = A;
     a.status = ctx->status;
     if (int rc = attach_fallback(ctx, &a)) return rc;
+    if (is_mask(&updates[0])) {
+      if (!(len % cfg->chunk_size == 0 && tc_enabled() && tc3_supported(ChunkMode::MergeAdam, a)))
+        return fail(DMB_PROTOCOL, "mask-format updates need the tensor-core merge path (s = 64, whole chunks)");
+      a.geo.wire_mask = 1;
+    }
     launch_chunk_kernel(ChunkMode::MergeAdam, a, s);
     return last_launch();
   }
@@ -938,6 +1012,13 @@ int dmb_kernel_timer_read(double* total_ms, uint64_t* launches) {
   g_timer_pairs.clear();
   if (total_ms) *total_ms = t;
   if (launches) *launches = n;
+  return DMB_OK;
+}
+
+int dmb_set_wire_format(dmb_ctx* ctx, int32_t format) {
+  if (!ctx) return fail(DMB_CONFIG, "ctx is NULL");
+  if (format != DMB_WIRE_REFERENCE && format != DMB_WIRE_MASK) return fail(DMB_CONFIG, "unknown wire format %d", format);
+  ctx->wire_format = format;
   return DMB_OK;
 }
 

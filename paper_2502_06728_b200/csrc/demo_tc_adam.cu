@@ -361,6 +361,22 @@ __device__ __forceinline__ float cond_w(float c) {
 // exact TF32 split: hi keeps the top 10 mantissa bits, lo = x - hi is exact in FP32
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
+// MASK bodies with 2-bit values and k in {8, 16, 32}: a chunk's codes are one aligned
+// 16/32/64-bit word (code 1: +1, 2: -1, 0: zero; LSB first, replicate.cpp:340-352)
+__device__ __forceinline__ bool word_codes(int k) { return k == 8 || k == 16 || k == 32; }
+__device__ __forceinline__ uint32_t code_of(float w) { return w > 0.0f ? 1u : (w < 0.0f ? 2u : 0u); }
+__device__ __forceinline__ float value_of(uint32_t code) { return code == 1u ? 1.0f : (code == 2u ? -1.0f : 0.0f); }
+__device__ __forceinline__ void store_code_word(uint8_t* vals, uint64_t row, int k, uint64_t w) {
+  if (k == 32) reinterpret_cast<uint64_t*>(vals)[row] = w;
+  else if (k == 16) reinterpret_cast<uint32_t*>(vals)[row] = (uint32_t)w;
+  else reinterpret_cast<uint16_t*>(vals)[row] = (uint16_t)w;
+}
+__device__ __forceinline__ uint64_t load_code_word(const uint8_t* vals, uint64_t row, int k) {
+  if (k == 32) return __ldg(reinterpret_cast<const unsigned long long*>(vals) + row);
+  if (k == 16) return __ldg(reinterpret_cast<const unsigned int*>(vals) + row);
+  return __ldg(reinterpret_cast<const unsigned short*>(vals) + row);
+}
+
 struct TensorMaps {
   CUtensorMap g, p_in, ea_in, es_in, p_out, ea_out, es_out;
 };
@@ -690,6 +706,7 @@ __global__ void __maxnreg__(128)
 
       uint32_t sel0 = 0, sel1 = 0;
       bool def0 = false, def1 = false;
+      float gq0[16], gq1[16];  // merge, MASK bodies: this thread's grid entries
       if (!kMerge) {
         // ---- TopK of both rows (warp-uniform trip count) ----
         if (full_band) {
@@ -749,7 +766,8 @@ __global__ void __maxnreg__(128)
         }
         evt(a, tid == 0, it, 6);
         evt_at(a, lane == 0, it, 16 + warp);
-        // ---- payload: indices ascending, then values (replicate.cpp:316-356) ----
+        // ---- payload: indices ascending, then values (replicate.cpp:316-356); MASK layout:
+        // one u64 mask per chunk, then the values (2-bit codes when signs travel) ----
         if (a.body) {
           const uint64_t q0m = spread(sel0, s), q1m = spread(sel1, s);
           uint64_t all0 = q0m, all1 = q1m;
@@ -757,27 +775,99 @@ __global__ void __maxnreg__(128)
           all1 |= shfl64(all1, (lane & 28) | ((lane + 1) & 3));
           all0 |= shfl64(all0, (lane & 28) | ((lane + 2) & 3));
           all1 |= shfl64(all1, (lane & 28) | ((lane + 2) & 3));
+          const bool mask_wire = a.geo.wire_mask != 0;
+          const int vd = mask_wire ? mask_value_dtype(a.geo) : dtype;
           uint32_t* idx = reinterpret_cast<uint32_t*>(a.body);
-          uint8_t* vals = a.body + nvals * 4;
+          uint8_t* vals = a.body + (mask_wire ? nchunks * 8 : nvals * 4);
+          if (mask_wire && s == 0) {
+            if (act0 && !def0) reinterpret_cast<uint64_t*>(a.body)[r0] = all0;
+            if (act1 && !def1) reinterpret_cast<uint64_t*>(a.body)[r1] = all1;
+          }
+          const bool words = mask_wire && vd == DMB_TERNARY && word_codes(k);
+          if (words) {  // the row's codes assembled across the quad, one aligned store
+            uint64_t w0 = 0, w1 = 0;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
+            for (int e = 0; e < 16; ++e) {
+              const uint64_t below = (1ull << qcol(e, s)) - 1ull;
+              if ((sel0 >> e) & 1u) w0 |= (uint64_t)code_of(cond_w<WIRE>(c0[e])) << (2 * __popcll(all0 & below));
+              if ((sel1 >> e) & 1u) w1 |= (uint64_t)code_of(cond_w<WIRE>(c1[e])) << (2 * __popcll(all1 & below));
+            }
+            w0 |= shfl64(w0, (lane & 28) | ((lane + 1) & 3));
+            w1 |= shfl64(w1, (lane & 28) | ((lane + 1) & 3));
+            w0 |= shfl64(w0, (lane & 28) | ((lane + 2) & 3));
+            w1 |= shfl64(w1, (lane & 28) | ((lane + 2) & 3));
+            if (s == 0) {
+              if (act0 && !def0) store_code_word(vals, r0, k, w0);
+              if (act1 && !def1) store_code_word(vals, r1, k, w1);
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < 16 && !words; ++e) {
             const int col = qcol(e, s);
             const uint64_t below = (1ull << col) - 1ull;
             if (act0 && !def0 && ((sel0 >> e) & 1u)) {
               const uint64_t t = r0 * (uint64_t)k + __popcll(all0 & below);
-              idx[t] = (uint32_t)col;
-              store_wire_value(vals, t, cond_w<WIRE>(c0[e]), dtype);
+              if (!mask_wire) idx[t] = (uint32_t)col;
+              store_wire_value(vals, t, cond_w<WIRE>(c0[e]), vd);
             }
             if (act1 && !def1 && ((sel1 >> e) & 1u)) {
               const uint64_t t = r1 * (uint64_t)k + __popcll(all1 & below);
-              idx[t] = (uint32_t)col;
-              store_wire_value(vals, t, cond_w<WIRE>(c1[e]), dtype);
+              if (!mask_wire) idx[t] = (uint32_t)col;
+              store_wire_value(vals, t, cond_w<WIRE>(c1[e]), vd);
             }
           }
         }
       } else {
-        // ---- merge: the R gathered payloads in member order (replicate.cpp:282-300) into
-        // this warp's grid [16][64] (column XOR (row & 7) << 3), own selection ----
+        // ---- merge: the R gathered payloads in member order (replicate.cpp:282-300) ----
+        if (a.geo.wire_mask) {
+          // MASK bodies: every quad thread rebuilds its own 2 x 16 grid entries in registers
+          // from the rows' masks and values (value number = popc of the mask below the bit)
+          const int vd = mask_value_dtype(a.geo);
+          const bool words = vd == DMB_TERNARY && word_codes(k);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) gq0[e] = gq1[e] = 0.0f;
+          uint64_t om0 = 0, om1 = 0;
+          auto fetch = [&](int rr, uint64_t& m0, uint64_t& m1, uint64_t& w0, uint64_t& w1) {
+            const uint64_t* mk = reinterpret_cast<const uint64_t*>(a.in.body[rr]);
+            const uint8_t* vals = a.in.body[rr] + nchunks * 8;
+            m0 = act0 ? __ldg(reinterpret_cast<const unsigned long long*>(mk) + r0) : 0ull;
+            m1 = act1 ? __ldg(reinterpret_cast<const unsigned long long*>(mk) + r1) : 0ull;
+            w0 = (words && act0) ? load_code_word(vals, r0, k) : 0ull;
+            w1 = (words && act1) ? load_code_word(vals, r1, k) : 0ull;
+          };
+          uint64_t m0, m1, w0, w1;
+          fetch(0, m0, m1, w0, w1);
+          for (int rr = 0; rr < a.in.R; ++rr) {
+            uint64_t n0 = 0, n1 = 0, x0 = 0, x1 = 0;
+            if (rr + 1 < a.in.R) fetch(rr + 1, n0, n1, x0, x1);  // next member in flight
+            const uint8_t* vals = a.in.body[rr] + nchunks * 8;
+            if (s == 0 && ((act0 && __popcll(m0) != k) || (act1 && __popcll(m1) != k)))
+              atomicExch(&a.status->protocol_error, 1u);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int col = qcol(e, s);
+              const uint64_t below = (1ull << col) - 1ull;
+              if ((m0 >> col) & 1ull) {
+                const int t = __popcll(m0 & below);
+                gq0[e] += words ? value_of((uint32_t)(w0 >> (2 * t)) & 3u) : load_wire_value(vals, r0 * (uint64_t)k + t, vd);
+              }
+              if ((m1 >> col) & 1ull) {
+                const int t = __popcll(m1 & below);
+                gq1[e] += words ? value_of((uint32_t)(w1 >> (2 * t)) & 3u) : load_wire_value(vals, r1 * (uint64_t)k + t, vd);
+              }
+            }
+            if (rr == a.own_rank) {
+              om0 = m0;
+              om1 = m1;
+            }
+            m0 = n0;
+            m1 = n1;
+            w0 = x0;
+            w1 = x1;
+          }
+          sel0 = act0 ? gather16(om0, s) : 0u;
+          sel1 = act1 ? gather16(om1, s) : 0u;
+        } else {
         float* grid = reinterpret_cast<float*>(scr);
 #pragma unroll
         for (int j = 0; j < 32; ++j) grid[lane + 32 * j] = 0.0f;
@@ -821,6 +911,7 @@ __global__ void __maxnreg__(128)
         __syncwarp();
         sel0 = act0 ? gather16(own0, s) : 0u;
         sel1 = act1 ? gather16(own1, s) : 0u;
+        }
       }
 
       if (!kEncodeOnly) {
@@ -835,8 +926,10 @@ __global__ void __maxnreg__(128)
           const bool on0 = (sel0 >> e) & 1u, on1 = (sel1 >> e) & 1u;
           float v0, v1;
           if (kMerge) {
-            v0 = grid[l0 * S + (col ^ ((l0 & 7) << 3))] * invR - ((on0 && !full_band) ? c0[e] : 0.0f);
-            v1 = grid[l1 * S + (col ^ ((l1 & 7) << 3))] * invR - ((on1 && !full_band) ? c1[e] : 0.0f);
+            const float g0v = a.geo.wire_mask ? gq0[e] : grid[l0 * S + (col ^ ((l0 & 7) << 3))];
+            const float g1v = a.geo.wire_mask ? gq1[e] : grid[l1 * S + (col ^ ((l1 & 7) << 3))];
+            v0 = g0v * invR - ((on0 && !full_band) ? c0[e] : 0.0f);
+            v1 = g1v * invR - ((on1 && !full_band) ? c1[e] : 0.0f);
           } else {
             v0 = full_band ? cond_w<WIRE>(c0[e]) : (on0 ? cond_w<WIRE>(c0[e]) - c0[e] : 0.0f);
             v1 = full_band ? cond_w<WIRE>(c1[e]) : (on1 ? cond_w<WIRE>(c1[e]) - c1[e] : 0.0f);
@@ -966,21 +1059,32 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
     const float c0f = (float)cd0, c1f = (float)cd1;
     const float w0 = sel0 ? condition_f64(cd0, dtype, sign_mode) : 0.0f;
     const float w1 = sel1 ? condition_f64(cd1, dtype, sign_mode) : 0.0f;
-    // payload: ascending frequency
+    // payload: ascending frequency (MASK layout: u64 mask, then the values)
     if (a.body) {
       const unsigned m0 = __ballot_sync(kFull, sel0), m1 = __ballot_sync(kFull, sel1);
       const unsigned lt = lanemask_lt();
+      const bool mask_wire = a.geo.wire_mask != 0;
+      const int vd = mask_wire ? mask_value_dtype(a.geo) : dtype;
       uint32_t* idx = reinterpret_cast<uint32_t*>(a.body);
-      uint8_t* vals = a.body + nvals * 4;
+      uint8_t* vals = a.body + (mask_wire ? a.geo.nchunks * 8 : nvals * 4);
+      if (mask_wire && lane == 0) reinterpret_cast<uint64_t*>(a.body)[c] = ((uint64_t)m1 << 32) | m0;
+      if (mask_wire && vd == DMB_TERNARY && word_codes(k)) {
+        uint64_t w = 0;
+        if (sel0) w |= (uint64_t)code_of(w0) << (2 * __popc(m0 & lt));
+        if (sel1) w |= (uint64_t)code_of(w1) << (2 * (__popc(m0) + __popc(m1 & lt)));
+        w = ((uint64_t)__reduce_or_sync(kFull, (uint32_t)(w >> 32)) << 32) | __reduce_or_sync(kFull, (uint32_t)w);
+        if (lane == 0) store_code_word(vals, c, k, w);
+      } else {
       if (sel0) {
         const uint64_t t = c * (uint64_t)k + __popc(m0 & lt);
-        idx[t] = (uint32_t)lane;
-        store_wire_value(vals, t, w0, dtype);
+        if (!mask_wire) idx[t] = (uint32_t)lane;
+        store_wire_value(vals, t, w0, vd);
       }
       if (sel1) {
         const uint64_t t = c * (uint64_t)k + __popc(m0) + __popc(m1 & lt);
-        idx[t] = (uint32_t)(lane + 32);
-        store_wire_value(vals, t, w1, dtype);
+        if (!mask_wire) idx[t] = (uint32_t)(lane + 32);
+        store_wire_value(vals, t, w1, vd);
+      }
       }
     }
     if (kEncodeOnly) continue;

@@ -111,7 +111,12 @@ struct DemoGeometry {
   int s, k;            // chunk_size, top_k
   int dtype;           // transfer dtype
   bool sign_mode;
+  int wire_mask;       // DMB_WIRE_MASK bodies (tensor-core AdamW kernels only)
 };
+// MASK body: u64 masks, then values (2-bit codes when signs travel)
+__device__ __forceinline__ int mask_value_dtype(const DemoGeometry& g) {
+  return (g.sign_mode || g.dtype == DMB_TERNARY) ? DMB_TERNARY : g.dtype;
+}
 
 // Device basis tables for one chunk size (host-computed FP64 with libm cos,
 // transform.cpp:41-54; FP32 copies are rounded from it).

@@ -500,12 +500,14 @@ def test_tc_fused_step_matches_oracle(oracle, monkeypatch, opt_kind, force):
     assert np.array_equal(idx, want["freq_indices"])
 
 
-@pytest.mark.parametrize("k,force", [(32, False), (8, False), (32, True)])
-def test_tc_cluster_adamw_prepare_merge_matches_oracle(oracle, monkeypatch, k, force):
+@pytest.mark.parametrize("k,force,wire,sign", [(32, False, 0, True), (8, False, 0, True), (32, True, 0, True),
+                                               (32, False, 1, True), (8, True, 1, True), (16, False, 1, False)])
+def test_tc_cluster_adamw_prepare_merge_matches_oracle(oracle, monkeypatch, k, force, wire, sign):
     """The N>1 path as cluster.py drives it: dmb_adamw_prepare (no local_q: the tensor-core
     encode kernel) on R members' gradients, then dmb_merge_apply_adamw of the R bodies for one
     member (the tensor-core merge kernel) -- payloads and state against the oracle's
-    select_and_encode / decode_and_merge / adamw_apply (cluster.cpp:193-231)."""
+    select_and_encode / decode_and_merge / adamw_apply (cluster.cpp:193-231).  wire=1: the
+    MASK exchange layout, whose serialize() must still be the reference's bytes."""
     import ctypes as C
 
     from paper_2502_06728_b200 import _capi
@@ -516,13 +518,14 @@ def test_tc_cluster_adamw_prepare_merge_matches_oracle(oracle, monkeypatch, k, f
     if force:
         monkeypatch.setenv("DMB_FORCE_FP64", "1")
     lib = _capi.lib
-    n = 64 * 128 * 6 + 64 * 3 + 7  # partial last tile and chunk
+    n = 64 * 128 * 6 + 64 * 3 + (0 if wire else 7)  # partial last tile (and chunk: reference layout)
     R, own, step, lr = 3, 1, 5, 0.002
     rng = np.random.default_rng(31 + k)
     gs = [(rng.standard_normal(n) * 1e-3).astype(np.float32) for _ in range(R)]
-    rep = Rep(scheme=DEMO, chunk_size=64, top_k=k, compression=k / 64, sign_mode=True, seed=1234)
+    rep = Rep(scheme=DEMO, chunk_size=64, top_k=k, compression=k / 64, sign_mode=sign, seed=1234)
     c = rep_to_cfg(rep).c()
     cap = int(lib.dmb_update_capacity(C.byref(c), n))
+    assert lib.dmb_set_wire_format(context().h, wire) == 0
     ups = (_capi.Update * R)()
     keep = []
     wants = []
@@ -536,11 +539,19 @@ def test_tc_cluster_adamw_prepare_merge_matches_oracle(oracle, monkeypatch, k, f
         p.status()
         want = oracle.select_and_encode(gs[r].astype(np.float64), rep, step, 0)
         wants.append(want)
+        assert hdr.wire_format == (0 if not wire else (2 if sign else 1))
+        ser = (C.c_uint8 * (9 + cap))()
+        written = C.c_uint64(0)
+        assert lib.dmb_serialize(C.byref(hdr), 0, ser, 9 + cap, C.byref(written), _stream()) == 0, lib.dmb_last_error()
+        raw = bytes(ser)[: written.value]
         ni = want["freq_indices"].size
-        idx = body[: 4 * ni].view(torch.int32).cpu().numpy().astype(np.uint32)
+        idx = np.frombuffer(raw[9: 9 + 4 * ni], dtype=np.uint32)
         assert np.array_equal(idx, want["freq_indices"]), f"member {r} indices"
-        vals = body[4 * ni: 8 * ni].view(torch.float32).cpu().numpy()
-        assert np.array_equal(vals, want["values"].astype(np.float32)), f"member {r} values"
+        vals = np.frombuffer(raw[9 + 4 * ni: 9 + 8 * ni], dtype=np.float32)
+        if sign:
+            assert np.array_equal(vals, want["values"].astype(np.float32)), f"member {r} values"
+        else:
+            chunk_close(vals.astype(np.float64), want["values"], k, what=f"member {r} values")
         ups[r] = hdr
         keep += [gd, body]
     p0 = (rng.standard_normal(n) * 0.02).astype(np.float32)
@@ -551,6 +562,7 @@ def test_tc_cluster_adamw_prepare_merge_matches_oracle(oracle, monkeypatch, k, f
     steps = C.c_uint64(4)
     rc = lib.dmb_merge_apply_adamw(context().h, ups, R, own, C.byref(c), _ptr(pd), _ptr(ead), _ptr(esd),
                                    C.byref(steps), _ptr(god), n, step, C.byref(o), lr, _stream())
+    assert lib.dmb_set_wire_format(context().h, 0) == 0
     assert rc == 0, lib.dmb_last_error()
     p.status()
     q = oracle.decode_and_merge(rep, [w["values"] for w in wants], [w["freq_indices"] for w in wants], n, step, 0)
