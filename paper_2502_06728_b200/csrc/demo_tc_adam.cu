@@ -304,9 +304,11 @@ __device__ __forceinline__ void merge_desc(float (&a)[16]) {  // bitonic a[0..N)
       if (j > i) cas_desc(a[i], a[j]);
     }
 }
-__device__ __forceinline__ float kth_bitonic(const float (&c)[16], int k) {
+// returns the k-th largest |c| of the chunk; for k = 32 also the (k+1)-th (nxt), else nxt = -1
+__device__ __forceinline__ float kth_bitonic(const float (&c)[16], int k, float& nxt) {
   const int lane = threadIdx.x & 31;
   float a[16], p[16];
+  nxt = -1.0f;
 #pragma unroll
   for (int j = 0; j < 16; ++j) a[j] = fabsf(c[j]);
   sort16_desc(a);
@@ -322,9 +324,14 @@ __device__ __forceinline__ float kth_bitonic(const float (&c)[16], int k) {
     // top 32 of 64: sorted pair (0,1) against the reversed pair (3,2)
 #pragma unroll
     for (int i = 0; i < 16; ++i) p[i] = __shfl_sync(kFull, a[15 - i], lane ^ 3);
+    float n = 0.0f;  // the bottom 32 of the same merge: its maximum is the 33rd largest
 #pragma unroll
-    for (int i = 0; i < 16; ++i) m = fminf(m, fmaxf(a[i], p[i]));
+    for (int i = 0; i < 16; ++i) {
+      m = fminf(m, fmaxf(a[i], p[i]));
+      n = fmaxf(n, fminf(a[i], p[i]));
+    }
     m = fminf(m, __shfl_xor_sync(kFull, m, 1));
+    nxt = fmaxf(n, __shfl_xor_sync(kFull, n, 1));
   } else if (k == 16) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) p[i] = __shfl_sync(kFull, a[15 - i], lane ^ 1);
@@ -375,6 +382,38 @@ __device__ __forceinline__ uint64_t load_code_word(const uint8_t* vals, uint64_t
   if (k == 32) return __ldg(reinterpret_cast<const unsigned long long*>(vals) + row);
   if (k == 16) return __ldg(reinterpret_cast<const unsigned int*>(vals) + row);
   return __ldg(reinterpret_cast<const unsigned short*>(vals) + row);
+}
+
+// selection of a row from its threshold masks (gt: |c| > T, eq: |c| == T): everything
+// above T, then the lowest columns among the keys equal to T (ties toward the lower index)
+__device__ __forceinline__ uint32_t finish_sel(uint32_t gt, uint32_t eq, bool exact, int k, int s, bool active,
+                                               bool any_tie) {
+  uint32_t sel = exact ? (gt | eq) : gt;
+  if (any_tie) {  // warp-uniform
+    const int gt_all = quad_sum(__popc(gt));
+    uint64_t eq64 = spread(eq, s);
+    eq64 |= shfl64(eq64, (threadIdx.x & 28) | ((threadIdx.x + 1) & 3));
+    eq64 |= shfl64(eq64, (threadIdx.x & 28) | ((threadIdx.x + 2) & 3));
+    if (!exact) {
+      uint64_t pick = 0, m = eq64;
+      for (int n = k - gt_all; n > 0 && m; --n) {
+        pick |= m & (~m + 1ull);
+        m &= m - 1ull;
+      }
+      sel = gt | gather16(pick, s);
+    }
+  }
+  return active ? sel : 0u;
+}
+__device__ __forceinline__ void masks_at(const float (&c)[16], float T, uint32_t& gt, uint32_t& eq) {
+  gt = 0;
+  eq = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float m = fabsf(c[j]);
+    if (m > T) gt |= 1u << j;
+    if (m == T) eq |= 1u << j;
+  }
 }
 
 struct TensorMaps {
@@ -708,18 +747,25 @@ __global__ void __maxnreg__(128)
       bool def0 = false, def1 = false;
       float gq0[16], gq1[16];  // merge, MASK bodies: this thread's grid entries
       if (!kMerge) {
+        float kth0 = 0.f, kth1 = 0.f, nxt0 = 0.f, nxt1 = 0.f;  // k-th and (k+1)-th largest |c|
         // ---- TopK of both rows (warp-uniform trip count) ----
         if (full_band) {
           sel0 = act0 ? 0xffffu : 0u;
           sel1 = act1 ? 0xffffu : 0u;
         } else if (bitonic_k(k)) {
-          const float T0 = kth_bitonic(c0, k), T1 = kth_bitonic(c1, k);
-          RowSel q0{__float_as_uint(T0), true, false}, q1{__float_as_uint(T1), true, false};
-          q0.exact = quad_sum(count_ge16(c0, T0)) == k;
-          q1.exact = quad_sum(count_ge16(c1, T1)) == k;
-          const bool any_tie = __any_sync(kFull, (act0 && !q0.exact) || (act1 && !q1.exact));
-          sel0 = row_finish(q0, c0, k, s, act0, any_tie);
-          sel1 = row_finish(q1, c1, k, s, act1, any_tie);
+          float nx0, nx1;
+          const float T0 = kth_bitonic(c0, k, nx0), T1 = kth_bitonic(c1, k, nx1);
+          uint32_t gt0, eq0, gt1, eq1;
+          masks_at(c0, T0, gt0, eq0);
+          masks_at(c1, T1, gt1, eq1);
+          const bool ex0 = quad_sum(__popc(gt0 | eq0)) == k, ex1 = quad_sum(__popc(gt1 | eq1)) == k;
+          const bool any_tie = __any_sync(kFull, (act0 && !ex0) || (act1 && !ex1));
+          sel0 = finish_sel(gt0, eq0, ex0, k, s, act0, any_tie);
+          sel1 = finish_sel(gt1, eq1, ex1, k, s, act1, any_tie);
+          kth0 = T0;  // the smallest selected |c| is the k-th largest
+          kth1 = T1;
+          nxt0 = nx0;
+          nxt1 = nx1;
         } else {
           int top0, top1;
           RowSel q0 = row_start(c0, act0, top0), q1 = row_start(c1, act1, top1);
@@ -740,23 +786,26 @@ __global__ void __maxnreg__(128)
         // error bound cannot settle is handed whole to the FP64 fix-up kernel, which runs
         // after this one (re-deriving in the oracle's operation order off the critical path
         // is cheaper than stalling the tile pipeline for it) ----
-        auto certify = [&](const float (&c)[16], uint32_t sel, float l1, bool act) {
-          float kth = FLT_MAX, nxt = 0.f;
+        const bool have_kth = !full_band && bitonic_k(k), have_nxt = have_kth && k == 32;  // warp-uniform
+        auto certify = [&](const float (&c)[16], uint32_t sel, float l1, bool act, float kth, float nxt) {
+          if (!have_kth || !have_nxt) {
+            float kq = FLT_MAX, nq = 0.f;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float m = fabsf(c[j]);
-            if ((sel >> j) & 1u) kth = fminf(kth, m);
-            else nxt = fmaxf(nxt, m);
+            for (int j = 0; j < 16; ++j) {
+              const float m = fabsf(c[j]);
+              if ((sel >> j) & 1u) kq = fminf(kq, m);
+              else nq = fmaxf(nq, m);
+            }
+            if (!have_kth) kth = quad_min(kq);
+            if (!have_nxt) nxt = quad_max(nq);
           }
-          kth = quad_min(kth);
-          nxt = quad_max(nxt);
           const float eps = kEpsScale * l1;
           const bool sel_unc = !full_band && !(kth - nxt > 2.0f * eps);
           const bool sign_unc = need_signs && !(kth > eps);
           return act && !isnan(l1) && (sel_unc || sign_unc || a.force_fp64);
         };
-        def0 = certify(c0, sel0, l10, act0);
-        def1 = certify(c1, sel1, l11, act1);
+        def0 = certify(c0, sel0, l10, act0, kth0, nxt0);
+        def1 = certify(c1, sel1, l11, act1, kth1, nxt1);
         // a chunk handed to the FP64 fix-up kernel keeps a NaN-tagged W row so the apply
         // warps leave its state as loaded
         if (s == 0 && (def0 || def1)) {
