@@ -636,15 +636,7 @@ __global__ void __maxnreg__(128)
       front(tile + G, 1);
     }
     for (uint32_t it = 0; tile < ntiles; tile += G, ++it) {
-      if (tile + 2 * G < ntiles) {
-        // the X columns are free once the inverse of this tile (or, encode only, the
-        // forward of the next) has read them
-        if (!kEncodeOnly) mbar_wait(bar_i, it & 1);
-        else mbar_wait(bar_f, (it + 1) & 1);
-        tc_fence_after();
-        front(tile + 2 * G, it + 2);
-      }
-      if (kEncodeOnly) continue;
+      if (!kEncodeOnly) {
       evt(a, tid == 32 * kSelWarps, it, 10);
       mbar_wait(bar_i, it & 1);
       evt(a, tid == 32 * kSelWarps, it, 11);
@@ -702,6 +694,17 @@ __global__ void __maxnreg__(128)
       __syncwarp();
       if (lane == 0) mbar_arrive(bar_a);
       evt(a, tid == 32 * kSelWarps, it, 13);
+      }
+      // AdamW first: its store frees the staging tile for the next tile's state load, which
+      // then runs under this front
+      if (tile + 2 * G < ntiles) {
+        // the X columns are free once the inverse of this tile (or, encode only, the
+        // forward of the next) has read them
+        if (!kEncodeOnly) mbar_wait(bar_i, it & 1);
+        else mbar_wait(bar_f, (it + 1) & 1);
+        tc_fence_after();
+        front(tile + 2 * G, it + 2);
+      }
     }
     goto teardown;
   }
