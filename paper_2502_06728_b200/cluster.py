@@ -167,7 +167,8 @@ class HybridCluster:
             for lo, hi in zip(edges[:-1], edges[1:]):
                 cap = int(lib.dmb_update_capacity(C.byref(c), hi - lo))
                 nch = (hi - lo) // 64
-                xfer = cap if not self.mask_wire else ((8 * nch + (nch * rep.top_k * vbits + 7) // 8 + 15) // 16) * 16
+                body = 24 * nch if vbits == 2 else 8 * nch + (nch * rep.top_k * vbits + 7) // 8  # MASK(_SIGN)
+                xfer = cap if not self.mask_wire else ((body + 15) // 16) * 16
                 self.buckets.append(dict(lo=lo, hi=hi, cap=cap, xfer=xfer,
                                          own=torch.empty(cap, dtype=torch.uint8, device=self.device),
                                          gathered=torch.empty(topo.nodes * xfer, dtype=torch.uint8,

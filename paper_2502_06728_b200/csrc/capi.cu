@@ -313,6 +313,7 @@ int32_t body_value_dtype(const dmb_update* u, int32_t dtype) {
   return u->wire_format == DMB_WIRE_MASK_SIGN ? DMB_TERNARY : dtype;
 }
 uint64_t mask_body_bytes(const dmb_update* u, int32_t dtype) {
+  if (u->wire_format == DMB_WIRE_MASK_SIGN) return 24 * chunks_of(u);  // masks + codes by column
   return 8 * chunks_of(u) + (u->n_values * value_bits(body_value_dtype(u, dtype)) + 7) / 8;
 }
 
@@ -678,8 +679,8 @@ int dmb_serialize(const dmb_update* u, int32_t dtype, uint8_t* host_out, uint64_
         if (!(mk & 1)) continue;
         std::memcpy(idx + 4 * t, &j, 4);
         float v;
-        if (vd == DMB_TERNARY) {
-          const uint32_t code = (vin[t >> 2] >> (2 * (t & 3))) & 3u;
+        if (vd == DMB_TERNARY) {  // codes by column: 16 bytes per chunk
+          const uint32_t code = (vin[16 * c + (j >> 2)] >> (2 * (j & 3))) & 3u;
           v = code == 1u ? 1.0f : (code == 2u ? -1.0f : 0.0f);
         } else if (vd == DMB_FP16) {
           uint16_t h;
@@ -738,6 +739,21 @@ int dmb_deserialize(const uint8_t* buf, uint64_t size, int32_t dtype, const dmb_
 
 int dmb_update_values(const dmb_update* u, int32_t dtype, float* d_values, void* stream) {
   if (u->n_values == 0) return DMB_OK;
+  if (is_mask(u)) {  // inspection of an exchange-layout body: through the reference bytes
+    std::vector<uint8_t> hb(9 + wire_bytes(u->n_values, u->n_indices, dtype));
+    uint64_t written = 0;
+    if (int rc = dmb_serialize(u, dtype, hb.data(), hb.size(), &written, stream)) return rc;
+    std::vector<float> v(u->n_values);
+    const uint8_t* vin = hb.data() + 9 + u->n_indices * 4;
+    for (uint64_t t = 0; t < u->n_values; ++t) {
+      if (dtype == DMB_FP32) std::memcpy(&v[t], vin + 4 * t, 4);
+      else if (dtype == DMB_FP16) { uint16_t h; std::memcpy(&h, vin + 2 * t, 2); v[t] = half_to_float(h); }
+      else { const uint32_t code = (vin[t >> 2] >> (2 * (t & 3))) & 3u; v[t] = code == 1u ? 1.0f : (code == 2u ? -1.0f : 0.0f); }
+    }
+    DMB_CUDA_TRY(cudaMemcpyAsync(d_values, v.data(), v.size() * 4, cudaMemcpyHostToDevice, as_stream(stream)));
+    DMB_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+    return DMB_OK;
+  }
   launch_unpack_values(values_region(u), u->n_values, body_value_dtype(u, dtype), d_values, as_stream(stream));
   return last_launch();
 }

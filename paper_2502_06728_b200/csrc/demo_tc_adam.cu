@@ -368,20 +368,14 @@ __device__ __forceinline__ float cond_w(float c) {
 // exact TF32 split: hi keeps the top 10 mantissa bits, lo = x - hi is exact in FP32
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
-// MASK bodies with 2-bit values and k in {8, 16, 32}: a chunk's codes are one aligned
-// 16/32/64-bit word (code 1: +1, 2: -1, 0: zero; LSB first, replicate.cpp:340-352)
-__device__ __forceinline__ bool word_codes(int k) { return k == 8 || k == 16 || k == 32; }
+// MASK bodies with signs (DMB_WIRE_MASK_SIGN): after the masks, each chunk's 2-bit codes by
+// column (code 1: +1, 2: -1, 0: zero or not selected), columns 0-31 in the first u64, 32-63
+// in the second -- decoding is a shift per column, independent of k
 __device__ __forceinline__ uint32_t code_of(float w) { return w > 0.0f ? 1u : (w < 0.0f ? 2u : 0u); }
 __device__ __forceinline__ float value_of(uint32_t code) { return code == 1u ? 1.0f : (code == 2u ? -1.0f : 0.0f); }
-__device__ __forceinline__ void store_code_word(uint8_t* vals, uint64_t row, int k, uint64_t w) {
-  if (k == 32) reinterpret_cast<uint64_t*>(vals)[row] = w;
-  else if (k == 16) reinterpret_cast<uint32_t*>(vals)[row] = (uint32_t)w;
-  else reinterpret_cast<uint16_t*>(vals)[row] = (uint16_t)w;
-}
-__device__ __forceinline__ uint64_t load_code_word(const uint8_t* vals, uint64_t row, int k) {
-  if (k == 32) return __ldg(reinterpret_cast<const unsigned long long*>(vals) + row);
-  if (k == 16) return __ldg(reinterpret_cast<const unsigned int*>(vals) + row);
-  return __ldg(reinterpret_cast<const unsigned short*>(vals) + row);
+__device__ __forceinline__ void store_dense(uint8_t* vals, uint64_t row, uint64_t lo, uint64_t hi) {
+  reinterpret_cast<uint64_t*>(vals)[2 * row] = lo;
+  reinterpret_cast<uint64_t*>(vals)[2 * row + 1] = hi;
 }
 
 // selection of a row from its threshold masks (gt: |c| > T, eq: |c| == T): everything
@@ -835,22 +829,33 @@ __global__ void __maxnreg__(128)
             if (act0 && !def0) reinterpret_cast<uint64_t*>(a.body)[r0] = all0;
             if (act1 && !def1) reinterpret_cast<uint64_t*>(a.body)[r1] = all1;
           }
-          const bool words = mask_wire && vd == DMB_TERNARY && word_codes(k);
-          if (words) {  // the row's codes assembled across the quad, one aligned store
-            uint64_t w0 = 0, w1 = 0;
+          const bool words = mask_wire && vd == DMB_TERNARY;
+          if (words) {  // the rows' codes by column, assembled across the quad
+            uint64_t l0 = 0, h0 = 0, l1 = 0, h1 = 0;
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
-              const uint64_t below = (1ull << qcol(e, s)) - 1ull;
-              if ((sel0 >> e) & 1u) w0 |= (uint64_t)code_of(cond_w<WIRE>(c0[e])) << (2 * __popcll(all0 & below));
-              if ((sel1 >> e) & 1u) w1 |= (uint64_t)code_of(cond_w<WIRE>(c1[e])) << (2 * __popcll(all1 & below));
+              const int col = qcol(e, s);
+              const uint64_t c0v = (sel0 >> e) & 1u ? (uint64_t)code_of(cond_w<WIRE>(c0[e])) : 0ull;
+              const uint64_t c1v = (sel1 >> e) & 1u ? (uint64_t)code_of(cond_w<WIRE>(c1[e])) : 0ull;
+              if (col < 32) {
+                l0 |= c0v << (2 * col);
+                l1 |= c1v << (2 * col);
+              } else {
+                h0 |= c0v << (2 * (col - 32));
+                h1 |= c1v << (2 * (col - 32));
+              }
             }
-            w0 |= shfl64(w0, (lane & 28) | ((lane + 1) & 3));
-            w1 |= shfl64(w1, (lane & 28) | ((lane + 1) & 3));
-            w0 |= shfl64(w0, (lane & 28) | ((lane + 2) & 3));
-            w1 |= shfl64(w1, (lane & 28) | ((lane + 2) & 3));
+#pragma unroll
+            for (int o = 1; o <= 2; ++o) {
+              const int src = (lane & 28) | ((lane + o) & 3);
+              l0 |= shfl64(l0, src);
+              h0 |= shfl64(h0, src);
+              l1 |= shfl64(l1, src);
+              h1 |= shfl64(h1, src);
+            }
             if (s == 0) {
-              if (act0 && !def0) store_code_word(vals, r0, k, w0);
-              if (act1 && !def1) store_code_word(vals, r1, k, w1);
+              if (act0 && !def0) store_dense(vals, r0, l0, h0);
+              if (act1 && !def1) store_dense(vals, r1, l1, h1);
             }
           }
 #pragma unroll
@@ -875,23 +880,42 @@ __global__ void __maxnreg__(128)
           // MASK bodies: every quad thread rebuilds its own 2 x 16 grid entries in registers
           // from the rows' masks and values (value number = popc of the mask below the bit)
           const int vd = mask_value_dtype(a.geo);
-          const bool words = vd == DMB_TERNARY && word_codes(k);
 #pragma unroll
           for (int e = 0; e < 16; ++e) gq0[e] = gq1[e] = 0.0f;
+          if (vd == DMB_TERNARY) {
+            // codes by column: the thread's columns 8r + 2s + b sit at bits 16r + 4s + 2b
+            uint64_t om0 = 0, om1 = 0;
+            for (int rr = 0; rr < a.in.R; ++rr) {
+              const unsigned long long* mk = reinterpret_cast<const unsigned long long*>(a.in.body[rr]);
+              const unsigned long long* dv = reinterpret_cast<const unsigned long long*>(a.in.body[rr] + nchunks * 8);
+              const uint64_t lo0 = act0 ? __ldg(dv + 2 * r0) : 0ull, hi0 = act0 ? __ldg(dv + 2 * r0 + 1) : 0ull;
+              const uint64_t lo1 = act1 ? __ldg(dv + 2 * r1) : 0ull, hi1 = act1 ? __ldg(dv + 2 * r1 + 1) : 0ull;
+              if (rr == a.own_rank) {
+                om0 = act0 ? __ldg(mk + r0) : 0ull;
+                om1 = act1 ? __ldg(mk + r1) : 0ull;
+              }
+              const uint64_t a0 = lo0 >> (4 * s), b0 = hi0 >> (4 * s), a1 = lo1 >> (4 * s), b1 = hi1 >> (4 * s);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                const int r = e >> 1, sh = 16 * (r & 3) + 2 * (e & 1);
+                gq0[e] += value_of((uint32_t)((r < 4 ? a0 : b0) >> sh) & 3u);
+                gq1[e] += value_of((uint32_t)((r < 4 ? a1 : b1) >> sh) & 3u);
+              }
+            }
+            sel0 = act0 ? gather16(om0, s) : 0u;
+            sel1 = act1 ? gather16(om1, s) : 0u;
+          } else {
           uint64_t om0 = 0, om1 = 0;
-          auto fetch = [&](int rr, uint64_t& m0, uint64_t& m1, uint64_t& w0, uint64_t& w1) {
+          auto fetch = [&](int rr, uint64_t& m0, uint64_t& m1) {
             const uint64_t* mk = reinterpret_cast<const uint64_t*>(a.in.body[rr]);
-            const uint8_t* vals = a.in.body[rr] + nchunks * 8;
             m0 = act0 ? __ldg(reinterpret_cast<const unsigned long long*>(mk) + r0) : 0ull;
             m1 = act1 ? __ldg(reinterpret_cast<const unsigned long long*>(mk) + r1) : 0ull;
-            w0 = (words && act0) ? load_code_word(vals, r0, k) : 0ull;
-            w1 = (words && act1) ? load_code_word(vals, r1, k) : 0ull;
           };
-          uint64_t m0, m1, w0, w1;
-          fetch(0, m0, m1, w0, w1);
+          uint64_t m0, m1;
+          fetch(0, m0, m1);
           for (int rr = 0; rr < a.in.R; ++rr) {
-            uint64_t n0 = 0, n1 = 0, x0 = 0, x1 = 0;
-            if (rr + 1 < a.in.R) fetch(rr + 1, n0, n1, x0, x1);  // next member in flight
+            uint64_t n0 = 0, n1 = 0;
+            if (rr + 1 < a.in.R) fetch(rr + 1, n0, n1);  // next member in flight
             const uint8_t* vals = a.in.body[rr] + nchunks * 8;
             if (s == 0 && ((act0 && __popcll(m0) != k) || (act1 && __popcll(m1) != k)))
               atomicExch(&a.status->protocol_error, 1u);
@@ -899,14 +923,8 @@ __global__ void __maxnreg__(128)
             for (int e = 0; e < 16; ++e) {
               const int col = qcol(e, s);
               const uint64_t below = (1ull << col) - 1ull;
-              if ((m0 >> col) & 1ull) {
-                const int t = __popcll(m0 & below);
-                gq0[e] += words ? value_of((uint32_t)(w0 >> (2 * t)) & 3u) : load_wire_value(vals, r0 * (uint64_t)k + t, vd);
-              }
-              if ((m1 >> col) & 1ull) {
-                const int t = __popcll(m1 & below);
-                gq1[e] += words ? value_of((uint32_t)(w1 >> (2 * t)) & 3u) : load_wire_value(vals, r1 * (uint64_t)k + t, vd);
-              }
+              if ((m0 >> col) & 1ull) gq0[e] += load_wire_value(vals, r0 * (uint64_t)k + __popcll(m0 & below), vd);
+              if ((m1 >> col) & 1ull) gq1[e] += load_wire_value(vals, r1 * (uint64_t)k + __popcll(m1 & below), vd);
             }
             if (rr == a.own_rank) {
               om0 = m0;
@@ -914,11 +932,10 @@ __global__ void __maxnreg__(128)
             }
             m0 = n0;
             m1 = n1;
-            w0 = x0;
-            w1 = x1;
           }
           sel0 = act0 ? gather16(om0, s) : 0u;
           sel1 = act1 ? gather16(om1, s) : 0u;
+          }
         } else {
         float* grid = reinterpret_cast<float*>(scr);
 #pragma unroll
@@ -1120,12 +1137,12 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
       uint32_t* idx = reinterpret_cast<uint32_t*>(a.body);
       uint8_t* vals = a.body + (mask_wire ? a.geo.nchunks * 8 : nvals * 4);
       if (mask_wire && lane == 0) reinterpret_cast<uint64_t*>(a.body)[c] = ((uint64_t)m1 << 32) | m0;
-      if (mask_wire && vd == DMB_TERNARY && word_codes(k)) {
-        uint64_t w = 0;
-        if (sel0) w |= (uint64_t)code_of(w0) << (2 * __popc(m0 & lt));
-        if (sel1) w |= (uint64_t)code_of(w1) << (2 * (__popc(m0) + __popc(m1 & lt)));
-        w = ((uint64_t)__reduce_or_sync(kFull, (uint32_t)(w >> 32)) << 32) | __reduce_or_sync(kFull, (uint32_t)w);
-        if (lane == 0) store_code_word(vals, c, k, w);
+      if (mask_wire && vd == DMB_TERNARY) {  // codes by column: lane j holds columns j and j+32
+        const uint64_t lo = sel0 ? (uint64_t)code_of(w0) << (2 * lane) : 0ull;
+        const uint64_t hi = sel1 ? (uint64_t)code_of(w1) << (2 * lane) : 0ull;
+        const uint64_t l = ((uint64_t)__reduce_or_sync(kFull, (uint32_t)(lo >> 32)) << 32) | __reduce_or_sync(kFull, (uint32_t)lo);
+        const uint64_t h = ((uint64_t)__reduce_or_sync(kFull, (uint32_t)(hi >> 32)) << 32) | __reduce_or_sync(kFull, (uint32_t)hi);
+        if (lane == 0) store_dense(vals, c, l, h);
       } else {
       if (sel0) {
         const uint64_t t = c * (uint64_t)k + __popc(m0 & lt);
