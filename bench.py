@@ -345,6 +345,20 @@ def run_ours(args, rank, world, local_rank):
                "d2h_bytes_per_step": 48, "ms_per_step": e_ms,
                "path": "pinned host gradient -> H2D -> dmb_step_*_local (C-ABI) -> dmb_status D2H"}
 
+    exchange = None
+    if distributed and cluster.ledger:
+        # per rank and step: bytes received in the replica all-gather (actual layout) beside
+        # the reference wire format's bytes for the same exchange (TrafficLedger model,
+        # cluster.cpp:16-61), and the shard-group reduce-scatter
+        tr = cluster.ledger[-1]
+        exchange = {"replica_group": cluster.topo.nodes, "shard_group": cluster.topo.accels_per_node,
+                    "wire": "mask" if cluster.mask_wire and cluster.buckets else "reference",
+                    "allgather_bytes_in": tr.inter_bytes,
+                    "allgather_bytes_in_reference_format": tr.inter_bytes_reference or tr.inter_bytes,
+                    "allgather_gbs_at_step_time": tr.inter_bytes / (ms * 1e-3) / 1e9,
+                    "reduce_scatter_bytes_ring_model": tr.intra_bytes,
+                    "buckets": len(cluster.buckets)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         n_threads = os.cpu_count() or 1
@@ -368,6 +382,7 @@ def run_ours(args, rank, world, local_rank):
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
             "per_gpu_params_per_s": shard_len / (ms * 1e-3),
             "model_params_per_s": L / (ms * 1e-3),
+            "exchange": exchange,
         }
         print(json.dumps(line), flush=True)
 
