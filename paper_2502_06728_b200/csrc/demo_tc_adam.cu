@@ -71,6 +71,11 @@ constexpr uint32_t SMEM_BYTES = OFF_L1 + 2 * TM * 4;
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
 constexpr uint32_t COL_C = 0, COL_D = 64, COL_XH = 128, COL_XL = 192, COL_G = 256;
+// StepSgd: the raw-gradient ring is not needed (the apply warps recompute m_acc from the
+// staged momentum and gradient); its columns hold W2 = wire on the selection (hi, lo) and
+// D2 = IDCT(W2) = Q, next to W1 = coef on the selection (X columns) and D1 = IDCT(W1) = local_q
+constexpr uint32_t COL_W2H = 256, COL_W2L = 320, COL_D2 = 384;
+constexpr uint32_t OFF_M = OFF_SCR;  // StepSgd: the momentum tile of the gradient split
 constexpr uint32_t TMEM_COLS = 512;
 
 // Certification radius of a tensor-core coefficient: |c_tc - c_oracle| <= kEpsScale ||x||_1.
@@ -419,6 +424,7 @@ __global__ void __maxnreg__(128)
     demo_tc_adam_kernel(const ChunkArgs a, const __grid_constant__ TensorMaps maps) {
   constexpr bool kEncodeOnly = MODE == ChunkMode::EncodeAdam;
   constexpr bool kMerge = MODE == ChunkMode::MergeAdam;
+  constexpr bool kSgd = MODE == ChunkMode::StepSgd;  // m = beta m + g; m -= local_q; p -= lr Q
 
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023u) != 0u) __trap();
@@ -496,7 +502,7 @@ __global__ void __maxnreg__(128)
         if (lane == 0) {
           const CUtensorMap* m[3] = {&maps.p_out, &maps.ea_out, &maps.es_out};
 #pragma unroll
-          for (int v = 0; v < 3; ++v) {
+          for (int v = 0; v < (kSgd ? 2 : 3); ++v) {  // SGD: p, m (the staged gradient is input only)
             tma_2d_store(m[v], 0, (int)(tile * TM), smem + OFF_ST + v * TILE);
             tma_2d_store(m[v], 32, (int)(tile * TM), smem + OFF_ST + v * TILE + BOX);
           }
@@ -517,9 +523,13 @@ __global__ void __maxnreg__(128)
     const uint32_t s_base = smem_u32(smem);
     auto load_g = [&](uint64_t t) {
       if (lane == 0) {
-        mbar_arrive_expect_tx(bar_g, TILE);
+        mbar_arrive_expect_tx(bar_g, kSgd ? 2 * TILE : TILE);
         tma_2d(smem + OFF_G, &maps.g, 0, (int)(t * TM), bar_g);
         tma_2d(smem + OFF_G + BOX, &maps.g, 32, (int)(t * TM), bar_g);
+        if (kSgd) {  // the momentum tile: m_acc = beta m + g is the vector encoded
+          tma_2d(smem + OFF_M, &maps.ea_in, 0, (int)(t * TM), bar_g);
+          tma_2d(smem + OFF_M + BOX, &maps.ea_in, 32, (int)(t * TM), bar_g);
+        }
       }
       __syncwarp();
     };
@@ -527,19 +537,20 @@ __global__ void __maxnreg__(128)
     // cross terms (hi*lo, lo*hi: |term| <= 2^-10 |x||B|) accumulate first and the 8 hi*hi
     // steps last, so the accumulator is small while the small terms are added: this is
     // what the certification radius kEpsScale assumes (see there).
-    auto issue = [&](uint32_t d, uint32_t bh, uint32_t bl, uint64_t* bar) {
+    auto issue = [&](uint32_t d, uint32_t bh, uint32_t bl, uint64_t* bar, uint32_t ah = COL_XH,
+                     uint32_t al = COL_XL) {
       tc_fence_after();
       if (lane == 0) {
         auto bo = [](int kk) { return (uint32_t)(kk >> 2) * (S * 128u) + (uint32_t)(kk & 3) * 32u; };
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          mma_tf32_ts(d, tmem + COL_XH + 8u * kk, desc_sw128(s_base + bl + bo(kk)), IDESC, kk > 0 ? 1u : 0u);
-          mma_tf32_ts(d, tmem + COL_XL + 8u * kk, desc_sw128(s_base + bh + bo(kk)), IDESC, 1u);
+          mma_tf32_ts(d, tmem + ah + 8u * kk, desc_sw128(s_base + bl + bo(kk)), IDESC, kk > 0 ? 1u : 0u);
+          mma_tf32_ts(d, tmem + al + 8u * kk, desc_sw128(s_base + bh + bo(kk)), IDESC, 1u);
         }
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          mma_tf32_ts(d, tmem + COL_XH + 8u * kk, desc_sw128(s_base + bh + bo(kk)), IDESC, 1u);
-        mma_commit(bar);
+          mma_tf32_ts(d, tmem + ah + 8u * kk, desc_sw128(s_base + bh + bo(kk)), IDESC, 1u);
+        if (bar) mma_commit(bar);
       }
       __syncwarp();
     };
@@ -562,7 +573,12 @@ __global__ void __maxnreg__(128)
         evt(a, tid == 32 * kMmaWarp, it, 14);
         if (it > 0) mbar_wait(bar_a, (it - 1) & 1);  // D of t-1 read by the apply warps
         evt(a, tid == 32 * kMmaWarp, it, 15);
-        issue(tmem + COL_D, OFF_BTHI, OFF_BTLO, bar_i);
+        if (kSgd) {  // local_q = IDCT(coef), Q = IDCT(wire), one commit for both
+          issue(tmem + COL_D, OFF_BTHI, OFF_BTLO, nullptr);
+          issue(tmem + COL_D2, OFF_BTHI, OFF_BTLO, bar_i, COL_W2H, COL_W2L);
+        } else {
+          issue(tmem + COL_D, OFF_BTHI, OFF_BTLO, bar_i);
+        }
       }
     }
     goto teardown;
@@ -591,11 +607,20 @@ __global__ void __maxnreg__(128)
           x[4 * e + 3] = v.w;
         }
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          l1 += fabsf(x[e]);
-          fin = fin && isfinite(x[e]);
+        for (int e = 0; e < 16; ++e) fin = fin && isfinite(x[e]);
+        if (kSgd) {  // m_acc = beta m + g, multiply then add (optim.cpp:27)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float4 m = *reinterpret_cast<const float4*>(smem + OFF_M + sw_off(trow, 4 * h + e));
+            x[4 * e] = __fadd_rn(__fmul_rn(a.sgd.beta, m.x), x[4 * e]);
+            x[4 * e + 1] = __fadd_rn(__fmul_rn(a.sgd.beta, m.y), x[4 * e + 1]);
+            x[4 * e + 2] = __fadd_rn(__fmul_rn(a.sgd.beta, m.z), x[4 * e + 2]);
+            x[4 * e + 3] = __fadd_rn(__fmul_rn(a.sgd.beta, m.w), x[4 * e + 3]);
+          }
         }
-        tmem_st16(tmem + tl + COL_G + 64 * (n % 3) + 16 * h, x);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) l1 += fabsf(x[e]);
+        if (!kSgd) tmem_st16(tmem + tl + COL_G + 64 * (n % 3) + 16 * h, x);
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           hi[e] = tf32_hi(x[e]);
@@ -638,6 +663,44 @@ __global__ void __maxnreg__(128)
       tc_fence_after();
       evt(a, tid == 32 * kSelWarps, it, 12);
       bool deferred = false;
+      if (kSgd) {
+#pragma unroll 1
+        for (int h = 0; h < 4; ++h) {
+          float d1[16], d2[16];
+          tmem_ld16(tmem + tl + COL_D + 16 * h, d1);
+          tmem_ld16(tmem + tl + COL_D2 + 16 * h, d2);
+          float4 p4[4], m4[4], g4[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t off = OFF_ST + sw_off(trow, 4 * h + e);
+            p4[e] = *reinterpret_cast<const float4*>(smem + off);
+            m4[e] = *reinterpret_cast<const float4*>(smem + off + TILE);
+            g4[e] = *reinterpret_cast<const float4*>(smem + off + 2 * TILE);
+          }
+          tmem_ld_wait();
+          if (h == 0) deferred = isnan(d1[0]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float* pz = &p4[e].x;
+            float* mz = &m4[e].x;
+            const float* gz = &g4[e].x;
+#pragma unroll
+            for (int z = 0; z < 4; ++z) {
+              const float macc = __fadd_rn(__fmul_rn(a.sgd.beta, mz[z]), gz[z]);
+              mz[z] = full_band ? 0.0f : macc - d1[4 * e + z];  // m -= local_q (k = s: local_q = m exactly)
+              pz[z] = pz[z] - a.sgd.lr * d2[4 * e + z];         // p -= lr Q (optim.cpp:45-49)
+            }
+          }
+          if (!deferred) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t off = OFF_ST + sw_off(trow, 4 * h + e);
+              *reinterpret_cast<float4*>(smem + off) = p4[e];
+              *reinterpret_cast<float4*>(smem + off + TILE) = m4[e];
+            }
+          }
+        }
+      } else
 #pragma unroll 1
       for (int h = 0; h < 4; ++h) {  // 16 columns at a time: every load of the quarter in flight together
         float d[16], g[16];
@@ -988,13 +1051,20 @@ __global__ void __maxnreg__(128)
         const float invR = kMerge ? 1.0f / (float)a.in.R : 1.0f;
         const float* grid = reinterpret_cast<const float*>(scr);
         const int l0 = lane >> 2, l1 = l0 + 8;
-        float w0[16], w1[16];
+        float w0[16], w1[16], u0[16], u1[16];  // SGD: u = W2 = wire on the selection
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int col = qcol(e, s);
           const bool on0 = (sel0 >> e) & 1u, on1 = (sel1 >> e) & 1u;
           float v0, v1;
-          if (kMerge) {
+          if (kSgd) {  // W1 = coef on the selection (local_q; k = s: unused), W2 = wire
+            v0 = (on0 && !full_band) ? c0[e] : 0.0f;
+            v1 = (on1 && !full_band) ? c1[e] : 0.0f;
+            const float x0 = full_band || on0 ? cond_w<WIRE>(c0[e]) : 0.0f;
+            const float x1 = full_band || on1 ? cond_w<WIRE>(c1[e]) : 0.0f;
+            u0[e] = def0 ? __int_as_float(0x7fc00000) : (act0 ? x0 : 0.0f);
+            u1[e] = def1 ? __int_as_float(0x7fc00000) : (act1 ? x1 : 0.0f);
+          } else if (kMerge) {
             const float g0v = a.geo.wire_mask ? gq0[e] : grid[l0 * S + (col ^ ((l0 & 7) << 3))];
             const float g1v = a.geo.wire_mask ? gq1[e] : grid[l1 * S + (col ^ ((l1 & 7) << 3))];
             v0 = g0v * invR - ((on0 && !full_band) ? c0[e] : 0.0f);
@@ -1022,6 +1092,19 @@ __global__ void __maxnreg__(128)
         st_quad(tmem + tq + COL_XH, r);
         pack_rows(w0, w1, r);
         st_quad(tmem + tq + COL_XL, r);
+        if (kSgd) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float h0 = tf32_hi(u0[e]), h1 = tf32_hi(u1[e]);
+            u0[e] -= h0;
+            u1[e] -= h1;
+            r[4 * (e >> 1) + (e & 1)] = __float_as_uint(h0);
+            r[4 * (e >> 1) + 2 + (e & 1)] = __float_as_uint(h1);
+          }
+          st_quad(tmem + tq + COL_W2H, r);
+          pack_rows(u0, u1, r);
+          st_quad(tmem + tq + COL_W2L, r);
+        }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -1053,6 +1136,7 @@ constexpr uint32_t FIX_SMEM = S * S * 8 + S * S * 4;  // FP64 basis (swizzled) +
 template <ChunkMode MODE, int WIRE>
 __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkArgs a) {
   constexpr bool kEncodeOnly = MODE == ChunkMode::EncodeAdam;
+  constexpr bool kSgd = MODE == ChunkMode::StepSgd;
   extern __shared__ __align__(16) uint8_t fsm[];
   double* b64 = reinterpret_cast<double*>(fsm);       // (j, i) at j*64 + (i ^ (j & 15))
   float* b32 = reinterpret_cast<float*>(fsm + S * S * 8);  // B[j][i] row-major
@@ -1075,7 +1159,11 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
   for (unsigned u = blockIdx.x * kFixWarps + (threadIdx.x >> 5); u < n; u += nwarps) {
     const uint64_t c = a.fb_list[u];
     const uint64_t g0 = c * S;
-    const float x0 = a.g[g0 + lane], x1 = a.g[g0 + lane + 32];
+    float x0 = a.g[g0 + lane], x1 = a.g[g0 + lane + 32];
+    if (kSgd) {  // the encoded vector is m_acc = beta m + g (multiply, then add)
+      x0 = __fadd_rn(__fmul_rn(a.sgd.beta, a.m_in[g0 + lane]), x0);
+      x1 = __fadd_rn(__fmul_rn(a.sgd.beta, a.m_in[g0 + lane + 32]), x1);
+    }
     // exact coefficients
     double cd0 = 0.0, cd1 = 0.0;
     const double* r0 = b64 + lane * S;
@@ -1157,6 +1245,31 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
       }
     }
     if (kEncodeOnly) continue;
+    if (kSgd) {  // local_q = IDCT(coef), Q = IDCT(wire) over the selection, ascending j
+      float q0 = 0.0f, q1 = 0.0f, l0 = 0.0f, l1 = 0.0f;
+      for (int e = 0; e < 2; ++e) {
+        unsigned m = __ballot_sync(kFull, e ? sel1 : sel0);
+        while (m) {
+          const int l = __ffs(m) - 1;
+          m &= m - 1;
+          const int j = l + 32 * e;
+          const float wj = __shfl_sync(kFull, e ? w1 : w0, l);
+          const float cj = __shfl_sync(kFull, e ? c1f : c0f, l);
+          q0 = fmaf(wj, b32[j * S + lane], q0);
+          q1 = fmaf(wj, b32[j * S + lane + 32], q1);
+          l0 = fmaf(cj, b32[j * S + lane], l0);
+          l1 = fmaf(cj, b32[j * S + lane + 32], l1);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const uint64_t gi = g0 + lane + 32 * e;
+        const float macc = e ? x1 : x0;
+        a.m_out[gi] = full_band ? 0.0f : macc - (e ? l1 : l0);
+        a.p_out[gi] = a.p_in[gi] - a.sgd.lr * (e ? q1 : q0);
+      }
+      continue;
+    }
     // D = IDCT(W), W = wire - coef on the selection (k = s: W = wire, D = Q)
     const float wd0 = full_band ? w0 : (sel0 ? w0 - c0f : 0.0f);
     const float wd1 = full_band ? w1 : (sel1 ? w1 - c1f : 0.0f);
@@ -1246,7 +1359,8 @@ void launch_mode(const ChunkArgs& a, const TensorMaps& maps, cudaStream_t stream
 
 bool tc3_supported(ChunkMode mode, const ChunkArgs& a) {
   if (a.geo.s != S || a.basis.Bhi == nullptr || encode_fn() == nullptr) return false;
-  if (!(mode == ChunkMode::StepAdam || mode == ChunkMode::MergeAdam || mode == ChunkMode::EncodeAdam))
+  if (!(mode == ChunkMode::StepAdam || mode == ChunkMode::MergeAdam || mode == ChunkMode::EncodeAdam ||
+        mode == ChunkMode::StepSgd))
     return false;
   if (a.local_q || a.m_accum || a.q_out) return false;  // inspection outputs: generic kernels
   if (a.geo.len / S == 0) return false;                 // the tensor maps need one whole chunk
@@ -1254,6 +1368,7 @@ bool tc3_supported(ChunkMode mode, const ChunkArgs& a) {
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
   if (!al(a.g)) return false;
   if (mode == ChunkMode::EncodeAdam) return true;
+  if (mode == ChunkMode::StepSgd) return a.m_in && a.m_out && al(a.m_in) && al(a.m_out) && al(a.p_in) && al(a.p_out);
   return al(a.p_in) && al(a.p_out) && al(a.ea_in) && al(a.ea_out) && al(a.es_in) && al(a.es_out);
 }
 
@@ -1263,7 +1378,13 @@ void launch_tc3_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) 
   memset(&maps, 0, sizeof(maps));
   const uint64_t rows = a.geo.len / S;
   tile_map(&maps.g, a.g, rows);
-  if (mode != ChunkMode::EncodeAdam) {
+  if (mode == ChunkMode::StepSgd) {  // staging: p, m, g; the split reads g and m
+    tile_map(&maps.p_in, a.p_in, rows);
+    tile_map(&maps.ea_in, a.m_in, rows);
+    tile_map(&maps.es_in, a.g, rows);
+    tile_map(&maps.p_out, a.p_out, rows);
+    tile_map(&maps.ea_out, a.m_out, rows);
+  } else if (mode != ChunkMode::EncodeAdam) {
     tile_map(&maps.p_in, a.p_in, rows);
     tile_map(&maps.ea_in, a.ea_in, rows);
     tile_map(&maps.es_in, a.es_in, rows);
@@ -1275,6 +1396,7 @@ void launch_tc3_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) 
     case ChunkMode::StepAdam: launch_mode<ChunkMode::StepAdam>(a, maps, stream); break;
     case ChunkMode::MergeAdam: launch_mode<ChunkMode::MergeAdam>(a, maps, stream); break;
     case ChunkMode::EncodeAdam: launch_mode<ChunkMode::EncodeAdam>(a, maps, stream); break;
+    case ChunkMode::StepSgd: launch_mode<ChunkMode::StepSgd>(a, maps, stream); break;
     default: break;
   }
 }
@@ -1305,6 +1427,11 @@ void launch_fix64_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream
       if (sign) go(demo_fix64_kernel<ChunkMode::EncodeAdam, kWireSign>);
       else if (f16) go(demo_fix64_kernel<ChunkMode::EncodeAdam, kWireF16>);
       else go(demo_fix64_kernel<ChunkMode::EncodeAdam, kWireF32>);
+      break;
+    case ChunkMode::StepSgd:
+      if (sign) go(demo_fix64_kernel<ChunkMode::StepSgd, kWireSign>);
+      else if (f16) go(demo_fix64_kernel<ChunkMode::StepSgd, kWireF16>);
+      else go(demo_fix64_kernel<ChunkMode::StepSgd, kWireF32>);
       break;
     default: break;  // MergeAdam never defers
   }

@@ -335,7 +335,9 @@ def test_fused_local_sgd_step_matches_stages(oracle):
                                       C.byref(o), C.byref(c), 4, 0, 0.01, C.byref(hdr), _stream())
     assert rc == 0
     p.status()
-    assert torch.equal(m_out, st.m)
+    # the fused step takes the tensor-core path (3xTF32 inverse for local_q), the staged one the
+    # SIMT kernel: the same selection, local_q within FP32 rounding of each other
+    chunk_close(host(m_out), host(st.m), 64, what="m_out")  # 1e-5 of the chunk's L-inf (the parity bar)
     assert torch.allclose(p_out, p_ref, rtol=0, atol=1e-7)
 
 
