@@ -374,7 +374,8 @@ def run_ours(args, rank, world, local_rank):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "kernel": ("demo_tc_adam_kernel<StepAdam> (tcgen05, warp-specialised)"
-                                    if args.optimizer == "adamw" else "demo_tc_kernel<StepSgd> (tcgen05)")
+                                    if args.optimizer == "adamw"
+                                    else "demo_tc_adam_kernel<StepSgd> (tcgen05, warp-specialised)")
                          if not distributed else "whole step incl. NCCL all-gather",
                          "kernel_ms": kern_ms, "kernel_launches": kern_n.value,
                          "step_achieved": step_achieved, "step_frac": step_achieved / hbm,

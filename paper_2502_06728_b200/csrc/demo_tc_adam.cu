@@ -156,7 +156,11 @@ __device__ __forceinline__ void pack_rows(const float (&c0)[16], const float (&c
   }
 }
 
+// pipeline event timestamps for tuning (dmb_debug_events); compiled in with -DDMB_KERNEL_EVENTS
 __device__ __forceinline__ void evt(const ChunkArgs& a, bool who, uint32_t it, int id) {
+#ifndef DMB_KERNEL_EVENTS
+  return;
+#endif
   if (a.dbg && who && blockIdx.x == 0 && it < 32) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -165,6 +169,9 @@ __device__ __forceinline__ void evt(const ChunkArgs& a, bool who, uint32_t it, i
 }
 
 __device__ __forceinline__ void evt_at(const ChunkArgs& a, bool who, uint32_t it, int slot) {
+#ifndef DMB_KERNEL_EVENTS
+  return;
+#endif
   if (a.dbg && who && blockIdx.x == 0 && it < 32) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
