@@ -440,9 +440,9 @@ __global__ void __maxnreg__(128)
   uint64_t* bar_f = bar_x + 1;  // forward DCT done (tcgen05.commit)
   uint64_t* bar_w = bar_f + 1;  // W in TMEM (select warps)
   uint64_t* bar_i = bar_w + 1;  // inverse DCT done (tcgen05.commit)
-  uint64_t* bar_s = bar_i + 1;  // optimizer state staged (TMA)
-  uint64_t* bar_a = bar_s + 1;  // AdamW written into the staging tile (apply warps)
-  uint64_t* bar_c = bar_a + 1;  // coefficient tile read out of TMEM (select warps)
+  uint64_t* bar_s = bar_i + 1;  // [2] optimizer state staged, per 32-column half (TMA)
+  uint64_t* bar_a = bar_s + 2;  // [2] that half written back into the staging tile (apply warps)
+  uint64_t* bar_c = bar_a + 2;  // coefficient tile read out of TMEM (select warps)
   uint64_t* bar_l = bar_c + 1;  // [2] ||x||_1 of tile n in l1buf[n & 1] (apply warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_l + 2);
   float* l1buf = reinterpret_cast<float*>(smem + OFF_L1);
@@ -469,8 +469,10 @@ __global__ void __maxnreg__(128)
     mbar_init(bar_f, 1);
     mbar_init(bar_w, kSelWarps);
     mbar_init(bar_i, 1);
-    mbar_init(bar_s, 1);
-    mbar_init(bar_a, kAppWarps);
+    mbar_init(&bar_s[0], 1);
+    mbar_init(&bar_s[1], 1);
+    mbar_init(&bar_a[0], kAppWarps);
+    mbar_init(&bar_a[1], kAppWarps);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, TMEM_COLS);
@@ -489,35 +491,38 @@ __global__ void __maxnreg__(128)
   const bool full_band = k == S;
   uint64_t tile = blockIdx.x;
 
-  auto load_state = [&](uint64_t t) {  // one thread
-    mbar_arrive_expect_tx(bar_s, 3 * TILE);
+  // the staging tile moves in two 32-column halves: the apply warps hand back the first
+  // half early, so its store and the next tile's first-half load start under the second
+  auto load_state = [&](uint64_t t, int h) {  // one thread
+    mbar_arrive_expect_tx(&bar_s[h], 3 * BOX);
     const CUtensorMap* m[3] = {&maps.p_in, &maps.ea_in, &maps.es_in};
 #pragma unroll
-    for (int v = 0; v < 3; ++v) {
-      tma_2d(smem + OFF_ST + v * TILE, m[v], 0, (int)(t * TM), bar_s);
-      tma_2d(smem + OFF_ST + v * TILE + BOX, m[v], 32, (int)(t * TM), bar_s);
-    }
+    for (int v = 0; v < 3; ++v) tma_2d(smem + OFF_ST + v * TILE + h * BOX, m[v], 32 * h, (int)(t * TM), &bar_s[h]);
   };
   // The two control warps stay converged: every lane runs the loop and the waits, lane 0
   // issues the TMA / tcgen05 operations.
   if (warp == kMemWarp) {
     // ===== state warp: p / exp_avg / exp_avg_sq through the staging tile =====
     if (!kEncodeOnly) {
-      if (tile < ntiles && lane == 0) load_state(tile);
+      if (tile < ntiles && lane == 0) {
+        load_state(tile, 0);
+        load_state(tile, 1);
+      }
       for (uint32_t it = 0; tile < ntiles; tile += G, ++it) {
-        mbar_wait(bar_a, it & 1);  // AdamW of this tile written into the staging tile
-        if (lane == 0) {
-          const CUtensorMap* m[3] = {&maps.p_out, &maps.ea_out, &maps.es_out};
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(&bar_a[h], it & 1);  // this half written back into the staging tile
+          if (lane == 0) {
+            const CUtensorMap* m[3] = {&maps.p_out, &maps.ea_out, &maps.es_out};
 #pragma unroll
-          for (int v = 0; v < (kSgd ? 2 : 3); ++v) {  // SGD: p, m (the staged gradient is input only)
-            tma_2d_store(m[v], 0, (int)(tile * TM), smem + OFF_ST + v * TILE);
-            tma_2d_store(m[v], 32, (int)(tile * TM), smem + OFF_ST + v * TILE + BOX);
+            for (int v = 0; v < (kSgd ? 2 : 3); ++v)  // SGD: p, m (the staged gradient is input only)
+              tma_2d_store(m[v], 32 * h, (int)(tile * TM), smem + OFF_ST + v * TILE + h * BOX);
+            bulk_commit();
+            bulk_wait_read();  // the half may be refilled
+            if (tile + G < ntiles) load_state(tile + G, h);
           }
-          bulk_commit();
-          bulk_wait_read();  // the staging tile may be refilled
-          if (tile + G < ntiles) load_state(tile + G);
+          __syncwarp();
         }
-        __syncwarp();
       }
       if (lane == 0) bulk_wait_all();
       __syncwarp();
@@ -578,7 +583,7 @@ __global__ void __maxnreg__(128)
       if (!kEncodeOnly) {
         mbar_wait(bar_w, it & 1);
         evt(a, tid == 32 * kMmaWarp, it, 14);
-        if (it > 0) mbar_wait(bar_a, (it - 1) & 1);  // D of t-1 read by the apply warps
+        if (it > 0) mbar_wait(&bar_a[1], (it - 1) & 1);  // D of t-1 read by the apply warps
         evt(a, tid == 32 * kMmaWarp, it, 15);
         if (kSgd) {  // local_q = IDCT(coef), Q = IDCT(wire), one commit for both
           issue(tmem + COL_D, OFF_BTHI, OFF_BTLO, nullptr);
@@ -666,7 +671,8 @@ __global__ void __maxnreg__(128)
       evt(a, tid == 32 * kSelWarps, it, 10);
       mbar_wait(bar_i, it & 1);
       evt(a, tid == 32 * kSelWarps, it, 11);
-      mbar_wait(bar_s, it & 1);
+      mbar_wait(&bar_s[0], it & 1);
+      mbar_wait(&bar_s[1], it & 1);
       tc_fence_after();
       evt(a, tid == 32 * kSelWarps, it, 12);
       bool deferred = false;
@@ -705,6 +711,12 @@ __global__ void __maxnreg__(128)
               *reinterpret_cast<float4*>(smem + off) = p4[e];
               *reinterpret_cast<float4*>(smem + off + TILE) = m4[e];
             }
+          }
+          if (h & 1) {  // half done: to the TMA store
+            tc_fence_before();
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_a[h >> 1]);
           }
         }
       } else
@@ -752,11 +764,13 @@ __global__ void __maxnreg__(128)
             *reinterpret_cast<float4*>(smem + off + 2 * TILE) = s4[e];
           }
         }
+        if (h & 1) {  // half done: to the TMA store
+          tc_fence_before();
+          fence_proxy_async_smem();  // generic writes -> the TMA store
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_a[h >> 1]);
+        }
       }
-      tc_fence_before();
-      fence_proxy_async_smem();  // generic writes -> the TMA store
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_a);
       evt(a, tid == 32 * kSelWarps, it, 13);
       }
       // AdamW first: its store frees the staging tile for the next tile's state load, which
