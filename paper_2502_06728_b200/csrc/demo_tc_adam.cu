@@ -1152,7 +1152,7 @@ teardown:
 // values, payload and W = wire - coef -> D = IDCT(W) -> AdamW as in the main kernel (whose
 // apply warps left this chunk's state untouched).
 constexpr int kFixWarps = 8;
-constexpr uint32_t FIX_SMEM = S * S * 8 + S * S * 4;  // FP64 basis (swizzled) + FP32 basis
+constexpr uint32_t FIX_SMEM = S * S * 8 + S * S * 4 + kFixWarps * S * 8;  // FP64 + FP32 basis, x per warp
 
 template <ChunkMode MODE, int WIRE>
 __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkArgs a) {
@@ -1161,6 +1161,7 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
   extern __shared__ __align__(16) uint8_t fsm[];
   double* b64 = reinterpret_cast<double*>(fsm);       // (j, i) at j*64 + (i ^ (j & 15))
   float* b32 = reinterpret_cast<float*>(fsm + S * S * 8);  // B[j][i] row-major
+  double* xw = reinterpret_cast<double*>(fsm + S * S * 12) + (threadIdx.x >> 5) * S;  // this warp's chunk
   if (*a.fb_count == 0) return;
   if (!kEncodeOnly && step_failed(a.status)) return;
   for (int u = threadIdx.x; u < S * S; u += blockDim.x) {
@@ -1190,9 +1191,13 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
     const double* r0 = b64 + lane * S;
     const double* r1 = b64 + (lane + 32) * S;
     const int sw = lane & 15;
+    __syncwarp();  // the previous chunk's reads of xw are done
+    xw[lane] = (double)x0;
+    xw[lane + 32] = (double)x1;
+    __syncwarp();
 #pragma unroll 8
     for (int i = 0; i < S; ++i) {
-      const double xi = (double)__shfl_sync(kFull, i < 32 ? x0 : x1, i & 31);
+      const double xi = xw[i];  // broadcast read
       cd0 = __dadd_rn(cd0, __dmul_rn(r0[i ^ sw], xi));
       cd1 = __dadd_rn(cd1, __dmul_rn(r1[i ^ sw], xi));
     }
@@ -1426,11 +1431,8 @@ void launch_tc3_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) 
 void launch_fix64_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) {
   count_launches(1);
   auto go = [&](auto kern) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FIX_SMEM);
-      attr = true;
-    }
+    // every instantiation needs its own attribute (a static flag here would be shared)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FIX_SMEM);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
