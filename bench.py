@@ -353,6 +353,7 @@ def run_ours(args, rank, world, local_rank):
         tr = cluster.ledger[-1]
         exchange = {"replica_group": cluster.topo.nodes, "shard_group": cluster.topo.accels_per_node,
                     "wire": "mask" if cluster.mask_wire and cluster.buckets else "reference",
+                    "gather": "copy engines over symmetric memory" if cluster.ce is not None else "nccl all_gather",
                     "allgather_bytes_in": tr.inter_bytes,
                     "allgather_bytes_in_reference_format": tr.inter_bytes_reference or tr.inter_bytes,
                     "allgather_gbs_at_step_time": tr.inter_bytes / (ms * 1e-3) / 1e9,

@@ -19,6 +19,7 @@ the reference's wire_bytes; `ledger` records them the way TrafficLedger does
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional
 
@@ -174,12 +175,38 @@ class HybridCluster:
                                          gathered=torch.empty(topo.nodes * xfer, dtype=torch.uint8,
                                                               device=self.device)))
             self.payload_bytes_per_param = sum(b["xfer"] for b in self.buckets) / L
+        self.ce = self._setup_ce_gather() if self.buckets else None
 
     def _reduce_scatter(self, grad_full: torch.Tensor) -> torch.Tensor:
         A = self.topo.accels_per_node
         if A == 1:
             return grad_full[: self.spec.extent]
         return reduce_scatter_mean(self.shard_grad, grad_full, A, self.shard_group)
+
+    def _setup_ce_gather(self):
+        """Copy-engine all-gather over symmetric memory: every member's bucket bodies live in
+        a buffer mapped into all replica-group members; after a device-side barrier each
+        member pulls the others' bodies with cudaMemcpyAsync (copy engines, no SMs), so the
+        exchange overlaps the persistent step kernels.  Two buffers alternate between steps,
+        so a member's next prepare never overwrites a body a peer is still copying.  Falls
+        back to the NCCL all-gather when symmetric memory is unavailable."""
+        if (self.topo.nodes < 2 or os.environ.get("DMB_CE_GATHER", "1") == "0"
+                or dist.get_backend(self.replica_group) != "nccl"):
+            return None
+        try:
+            import torch.distributed._symmetric_memory as symm
+
+            offs, total = [], 0
+            for b in self.buckets:
+                offs.append(total)
+                total += b["xfer"]
+            bufs = [symm.empty(total, dtype=torch.uint8, device=self.device) for _ in range(2)]
+            hdls = [symm.rendezvous(x, self.replica_group) for x in bufs]
+            if hdls[0].world_size != self.topo.nodes or hdls[0].rank != self.node:
+                return None
+            return dict(bufs=bufs, hdls=hdls, offs=offs, stream=torch.cuda.Stream(self.device), step=0)
+        except Exception:  # no symmetric-memory support here: NCCL all-gather
+            return None
 
     def _step_bucketed(self, step: int, lr: float, g_shard: torch.Tensor, tr: StepTraffic) -> None:
         R = self.topo.nodes
@@ -190,12 +217,18 @@ class HybridCluster:
         pending = []
 
         def merge(b, hdr, work):
-            work.wait()  # the compute stream waits for the gather; the host does not
+            own_ptr = None
+            if isinstance(work, tuple):  # copy-engine gather: (done event, own body)
+                torch.cuda.current_stream(self.device).wait_event(work[0])
+                own_ptr = work[1].data_ptr()
+            else:
+                work.wait()  # the compute stream waits for the gather; the host does not
             lo, hi = b["lo"], b["hi"]
             ups = (_capi.Update * R)()
             for r in range(R):
                 ups[r] = hdr
-                ups[r].body = b["gathered"][r * b["xfer"]:].data_ptr()
+                ups[r].body = own_ptr if (own_ptr is not None and r == self.node) else \
+                    b["gathered"][r * b["xfer"]:].data_ptr()
             if sgd:
                 _check(lib.dmb_merge_apply_sgd(ctx, ups, R, C.byref(c), _ptr(self.params[lo:hi]),
                                                _ptr(g_shard[lo:hi]), hi - lo, step, float(lr), st))
@@ -215,10 +248,16 @@ class HybridCluster:
                 lib.dmb_set_wire_format(ctx, 0)
 
     def _pipeline(self, step, lr, g_shard, tr, merge, pending, steps0, ctx, c, o, st, sgd, R):
-        for b in self.buckets:
+        ce = self.ce
+        if ce is not None:
+            par = ce["step"] & 1
+            ce["step"] += 1
+            cbuf, hdl, cs = ce["bufs"][par], ce["hdls"][par], ce["stream"]
+        for bi, b in enumerate(self.buckets):
             lo, hi = b["lo"], b["hi"]
             hdr = _capi.Update()
-            hdr.body = b["own"].data_ptr()
+            own = cbuf[ce["offs"][bi]: ce["offs"][bi] + b["xfer"]] if ce is not None else b["own"]
+            hdr.body = own.data_ptr()
             if sgd:
                 _check(lib.dmb_demo_sgd_prepare(ctx, _ptr(g_shard[lo:hi]), _ptr(self.m[lo:hi]), _ptr(self.m[lo:hi]),
                                                 hi - lo, C.byref(o), C.byref(c), step, self.accel, C.byref(hdr),
@@ -229,8 +268,22 @@ class HybridCluster:
             tr.inter_bytes += int(hdr.bytes) * (R - 1)
             tr.inter_bytes_reference += int(lib.dmb_wire_bytes(hdr.n_values, hdr.n_indices,
                                                                 self.rep.transfer_dtype)) * (R - 1)
-            work = dist.all_gather_into_tensor(b["gathered"], b["own"][: b["xfer"]], group=self.replica_group,
-                                               async_op=True)
+            if ce is not None:
+                ready = torch.cuda.Event()
+                ready.record(torch.cuda.current_stream(self.device))
+                cs.wait_event(ready)
+                with torch.cuda.stream(cs):
+                    hdl.barrier(channel=0)  # every member's prepare of this bucket is done
+                    for r in range(R):
+                        if r != self.node:
+                            b["gathered"][r * b["xfer"]:(r + 1) * b["xfer"]].copy_(
+                                hdl.get_buffer(r, (b["xfer"],), torch.uint8, ce["offs"][bi]), non_blocking=True)
+                    done = torch.cuda.Event()
+                    done.record(cs)
+                work = (done, own)
+            else:
+                work = dist.all_gather_into_tensor(b["gathered"], b["own"][: b["xfer"]], group=self.replica_group,
+                                                   async_op=True)
             if pending:
                 self.steps_b = C.c_uint64(steps0)
                 merge(*pending.pop())
