@@ -968,15 +968,42 @@ __global__ void __maxnreg__(128)
           for (int e = 0; e < 16; ++e) gq0[e] = gq1[e] = 0.0f;
           if (vd == DMB_TERNARY) {
             // codes by column: the thread's columns 8r + 2s + b sit at bits 16r + 4s + 2b
-            uint64_t om0 = 0, om1 = 0;
+            // up to 16 members: the warp's 16 rows of every member are copied into its scratch
+            // with cp.async at once (one memory latency), then decoded in member order
+            const unsigned long long* mko = reinterpret_cast<const unsigned long long*>(a.in.body[a.own_rank]);
+            const uint64_t om0 = act0 ? __ldg(mko + r0) : 0ull, om1 = act1 ? __ldg(mko + r1) : 0ull;
+            const bool staged = a.in.R <= 16;
+            uint64_t* stg = reinterpret_cast<uint64_t*>(scr);  // [member][row][lo, hi]
+            const uint64_t wrow = trow0 + base;
+            if (staged) {
+              for (int pr = lane; pr < a.in.R * 16; pr += 32) {
+                const int rr = pr >> 4, lr = pr & 15;
+                const uint64_t row = wrow + lr;
+                uint64_t* d = stg + 2 * pr;
+                if (row < nfull) {
+                  const uint8_t* src = a.in.body[rr] + nchunks * 8 + row * 16;
+                  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d)), "l"(src) : "memory");
+                  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + 1)), "l"(src + 8) : "memory");
+                }
+              }
+              asm volatile("cp.async.commit_group;" ::: "memory");
+              asm volatile("cp.async.wait_group 0;" ::: "memory");
+              __syncwarp();
+            }
+            const int q = lane >> 2;
             for (int rr = 0; rr < a.in.R; ++rr) {
-              const unsigned long long* mk = reinterpret_cast<const unsigned long long*>(a.in.body[rr]);
-              const unsigned long long* dv = reinterpret_cast<const unsigned long long*>(a.in.body[rr] + nchunks * 8);
-              const uint64_t lo0 = act0 ? __ldg(dv + 2 * r0) : 0ull, hi0 = act0 ? __ldg(dv + 2 * r0 + 1) : 0ull;
-              const uint64_t lo1 = act1 ? __ldg(dv + 2 * r1) : 0ull, hi1 = act1 ? __ldg(dv + 2 * r1 + 1) : 0ull;
-              if (rr == a.own_rank) {
-                om0 = act0 ? __ldg(mk + r0) : 0ull;
-                om1 = act1 ? __ldg(mk + r1) : 0ull;
+              uint64_t lo0, hi0, lo1, hi1;
+              if (staged) {
+                lo0 = act0 ? stg[2 * (rr * 16 + q)] : 0ull;
+                hi0 = act0 ? stg[2 * (rr * 16 + q) + 1] : 0ull;
+                lo1 = act1 ? stg[2 * (rr * 16 + q + 8)] : 0ull;
+                hi1 = act1 ? stg[2 * (rr * 16 + q + 8) + 1] : 0ull;
+              } else {
+                const unsigned long long* dv = reinterpret_cast<const unsigned long long*>(a.in.body[rr] + nchunks * 8);
+                lo0 = act0 ? __ldg(dv + 2 * r0) : 0ull;
+                hi0 = act0 ? __ldg(dv + 2 * r0 + 1) : 0ull;
+                lo1 = act1 ? __ldg(dv + 2 * r1) : 0ull;
+                hi1 = act1 ? __ldg(dv + 2 * r1 + 1) : 0ull;
               }
               const uint64_t a0 = lo0 >> (4 * s), b0 = hi0 >> (4 * s), a1 = lo1 >> (4 * s), b1 = hi1 >> (4 * s);
 #pragma unroll
@@ -986,6 +1013,7 @@ __global__ void __maxnreg__(128)
                 gq1[e] += value_of((uint32_t)((r < 4 ? a1 : b1) >> sh) & 3u);
               }
             }
+            if (staged) __syncwarp();  // the scratch is rewritten by the next tile
             sel0 = act0 ? gather16(om0, s) : 0u;
             sel1 = act1 ? gather16(om1, s) : 0u;
           } else {
