@@ -321,16 +321,17 @@ def run_ours(args, rank, world, local_rank):
     except Exception:
         pass
 
-    # ---- e2e: through the C-ABI with host buffers (pinned gradient in, status out) ----
+    # ---- e2e: through the public API with host buffers (pinned gradient in, status out) ----
+    # N=1: dmb_step_*_local (C ABI); N>1: HybridCluster.step on every rank, max over ranks
     e2e = None
-    if not args.no_e2e and not distributed:
+    if not args.no_e2e:
         host_g = torch.empty(L, dtype=torch.float32, pin_memory=True)
         host_g.copy_(grad)
         status_h = C.c_int64(-1)
         ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         e_steps = max(3, min(args.steps, 5))
         step_once(0)
-        torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
         ev2[0].record(stream)
         for k in range(e_steps):
@@ -341,9 +342,14 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         e_ms = max(ev2[0].elapsed_time(ev2[1]), wall * 1e3) / e_steps
-        e2e = {"value": L / (e_ms * 1e-3), "unit": "params/s", "h2d_bytes_per_step": 4 * L,
+        if distributed:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": world * shard_len / (e_ms * 1e-3), "unit": "params/s", "h2d_bytes_per_step": 4 * L,
                "d2h_bytes_per_step": 48, "ms_per_step": e_ms,
-               "path": "pinned host gradient -> H2D -> dmb_step_*_local (C-ABI) -> dmb_status D2H"}
+               "path": ("pinned host gradient -> H2D -> dmb_step_*_local (C-ABI) -> dmb_status D2H" if not distributed
+                        else "per rank: pinned host gradient -> H2D -> HybridCluster.step -> dmb_status D2H; max over ranks")}
 
     exchange = None
     if distributed and cluster.ledger:
