@@ -915,20 +915,27 @@ __global__ void __maxnreg__(128)
           }
           const bool words = mask_wire && vd == DMB_TERNARY;
           if (words) {  // the rows' codes by column, assembled across the quad
+            // element e = 2r + b of this thread is column 8r + 2s + b: its code goes to bit
+            // 16(r & 3) + 2b of the lo (r < 4) or hi word, then the word is shifted by 4s.
+            // For signs the code of cond(c) is the code of c itself: 1 if c > 0, 2 if c < 0
             uint64_t l0 = 0, h0 = 0, l1 = 0, h1 = 0;
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
-              const int col = qcol(e, s);
-              const uint64_t c0v = (sel0 >> e) & 1u ? (uint64_t)code_of(cond_w<WIRE>(c0[e])) : 0ull;
-              const uint64_t c1v = (sel1 >> e) & 1u ? (uint64_t)code_of(cond_w<WIRE>(c1[e])) : 0ull;
-              if (col < 32) {
-                l0 |= c0v << (2 * col);
-                l1 |= c1v << (2 * col);
+              const int r = e >> 1, sh = 16 * (r & 3) + 2 * (e & 1);
+              const uint32_t k0 = ((sel0 >> e) & 1u) ? ((uint32_t)(c0[e] > 0.0f) | ((uint32_t)(c0[e] < 0.0f) << 1)) : 0u;
+              const uint32_t k1 = ((sel1 >> e) & 1u) ? ((uint32_t)(c1[e] > 0.0f) | ((uint32_t)(c1[e] < 0.0f) << 1)) : 0u;
+              if (r < 4) {
+                l0 |= (uint64_t)k0 << sh;
+                l1 |= (uint64_t)k1 << sh;
               } else {
-                h0 |= c0v << (2 * (col - 32));
-                h1 |= c1v << (2 * (col - 32));
+                h0 |= (uint64_t)k0 << sh;
+                h1 |= (uint64_t)k1 << sh;
               }
             }
+            l0 <<= 4 * s;
+            h0 <<= 4 * s;
+            l1 <<= 4 * s;
+            h1 <<= 4 * s;
 #pragma unroll
             for (int o = 1; o <= 2; ++o) {
               const int src = (lane & 28) | ((lane + o) & 3);
