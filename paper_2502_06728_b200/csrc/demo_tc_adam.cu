@@ -292,19 +292,24 @@ __device__ __forceinline__ void cas_desc(float& x, float& y) {
   y = fminf(x, y);
   x = hi;
 }
+// 16-input sorting network of 60 compare-exchanges in 10 layers (Green's construction; the
+// bitonic network needs 80) -- checked exhaustively by the 0-1 principle in
+// tests/test_capi.py::test_sort16_network
+#define DMB_SORT16_NET(X)                                                                          \
+  X(0, 13) X(1, 12) X(2, 15) X(3, 14) X(4, 8) X(5, 6) X(7, 11) X(9, 10)                            \
+  X(0, 5) X(1, 7) X(2, 9) X(3, 4) X(6, 13) X(8, 14) X(10, 15) X(11, 12)                            \
+  X(0, 1) X(2, 3) X(4, 5) X(6, 8) X(7, 9) X(10, 11) X(12, 13) X(14, 15)                            \
+  X(0, 2) X(1, 3) X(4, 10) X(5, 11) X(6, 7) X(8, 9) X(12, 14) X(13, 15)                            \
+  X(1, 2) X(3, 12) X(4, 6) X(5, 7) X(8, 10) X(9, 11) X(13, 14)                                     \
+  X(1, 4) X(2, 6) X(5, 8) X(7, 10) X(9, 13) X(11, 14)                                              \
+  X(2, 4) X(3, 6) X(9, 12) X(11, 13)                                                               \
+  X(3, 5) X(6, 8) X(7, 9) X(10, 12)                                                                \
+  X(3, 4) X(5, 6) X(7, 8) X(9, 10) X(11, 12)                                                       \
+  X(6, 7) X(8, 9)
 __device__ __forceinline__ void sort16_desc(float (&a)[16]) {
-#pragma unroll
-  for (int size = 2; size <= 16; size <<= 1)
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1)
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int j = i ^ stride;
-        if (j > i) {
-          if ((i & size) == 0) cas_desc(a[i], a[j]);
-          else cas_desc(a[j], a[i]);
-        }
-      }
+#define DMB_CAS(i, j) cas_desc(a[i], a[j]);
+  DMB_SORT16_NET(DMB_CAS)
+#undef DMB_CAS
 }
 template <int N>
 __device__ __forceinline__ void merge_desc(float (&a)[16]) {  // bitonic a[0..N) -> descending
@@ -420,6 +425,14 @@ __device__ __forceinline__ void masks_at(const float (&c)[16], float T, uint32_t
     if (m > T) gt |= 1u << j;
     if (m == T) eq |= 1u << j;
   }
+}
+
+__device__ __forceinline__ uint32_t mask_ge(const float (&c)[16], float T) {
+  uint32_t ge = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (fabsf(c[j]) >= T) ge |= 1u << j;
+  return ge;
 }
 
 struct TensorMaps {
@@ -836,13 +849,20 @@ __global__ void __maxnreg__(128)
         } else if (bitonic_k(k)) {
           float nx0, nx1;
           const float T0 = kth_bitonic(c0, k, nx0), T1 = kth_bitonic(c1, k, nx1);
-          uint32_t gt0, eq0, gt1, eq1;
-          masks_at(c0, T0, gt0, eq0);
-          masks_at(c1, T1, gt1, eq1);
-          const bool ex0 = quad_sum(__popc(gt0 | eq0)) == k, ex1 = quad_sum(__popc(gt1 | eq1)) == k;
+          // |c| >= T selects exactly k unless keys tie at T (then the lowest columns win)
+          const uint32_t ge0 = mask_ge(c0, T0), ge1 = mask_ge(c1, T1);
+          const bool ex0 = quad_sum(__popc(ge0)) == k, ex1 = quad_sum(__popc(ge1)) == k;
           const bool any_tie = __any_sync(kFull, (act0 && !ex0) || (act1 && !ex1));
-          sel0 = finish_sel(gt0, eq0, ex0, k, s, act0, any_tie);
-          sel1 = finish_sel(gt1, eq1, ex1, k, s, act1, any_tie);
+          if (any_tie) {
+            uint32_t gt0, eq0, gt1, eq1;
+            masks_at(c0, T0, gt0, eq0);
+            masks_at(c1, T1, gt1, eq1);
+            sel0 = finish_sel(gt0, eq0, ex0, k, s, act0, true);
+            sel1 = finish_sel(gt1, eq1, ex1, k, s, act1, true);
+          } else {
+            sel0 = act0 ? ge0 : 0u;
+            sel1 = act1 ? ge1 : 0u;
+          }
           kth0 = T0;  // the smallest selected |c| is the k-th largest
           kth1 = T1;
           nxt0 = nx0;
@@ -916,34 +936,32 @@ __global__ void __maxnreg__(128)
           const bool words = mask_wire && vd == DMB_TERNARY;
           if (words) {  // the rows' codes by column, assembled across the quad
             // element e = 2r + b of this thread is column 8r + 2s + b: its code goes to bit
-            // 16(r & 3) + 2b of the lo (r < 4) or hi word, then the word is shifted by 4s.
-            // For signs the code of cond(c) is the code of c itself: 1 if c > 0, 2 if c < 0
-            uint64_t l0 = 0, h0 = 0, l1 = 0, h1 = 0;
+            // 16(r & 1) + 2b + 4s of 32-bit word r / 2 (columns 16(r / 2) .. +15). A stored row
+            // has every selected |c| above the certification radius, so c != 0 there and its
+            // code is 1 + the sign bit
+            uint32_t w0[4] = {0u, 0u, 0u, 0u}, w1[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
-              const int r = e >> 1, sh = 16 * (r & 3) + 2 * (e & 1);
-              const uint32_t k0 = ((sel0 >> e) & 1u) ? ((uint32_t)(c0[e] > 0.0f) | ((uint32_t)(c0[e] < 0.0f) << 1)) : 0u;
-              const uint32_t k1 = ((sel1 >> e) & 1u) ? ((uint32_t)(c1[e] > 0.0f) | ((uint32_t)(c1[e] < 0.0f) << 1)) : 0u;
-              if (r < 4) {
-                l0 |= (uint64_t)k0 << sh;
-                l1 |= (uint64_t)k1 << sh;
-              } else {
-                h0 |= (uint64_t)k0 << sh;
-                h1 |= (uint64_t)k1 << sh;
-              }
+              const int sh = 16 * ((e >> 1) & 1) + 2 * (e & 1);
+              w0[e >> 2] += (((sel0 >> e) & 1u) * (1u + (__float_as_uint(c0[e]) >> 31))) << sh;
+              w1[e >> 2] += (((sel1 >> e) & 1u) * (1u + (__float_as_uint(c1[e]) >> 31))) << sh;
             }
-            l0 <<= 4 * s;
-            h0 <<= 4 * s;
-            l1 <<= 4 * s;
-            h1 <<= 4 * s;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              w0[q] <<= 4 * s;
+              w1[q] <<= 4 * s;
+            }
 #pragma unroll
             for (int o = 1; o <= 2; ++o) {
               const int src = (lane & 28) | ((lane + o) & 3);
-              l0 |= shfl64(l0, src);
-              h0 |= shfl64(h0, src);
-              l1 |= shfl64(l1, src);
-              h1 |= shfl64(h1, src);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                w0[q] |= __shfl_sync(kFull, w0[q], src);
+                w1[q] |= __shfl_sync(kFull, w1[q], src);
+              }
             }
+            const uint64_t l0 = w0[0] | ((uint64_t)w0[1] << 32), h0 = w0[2] | ((uint64_t)w0[3] << 32);
+            const uint64_t l1 = w1[0] | ((uint64_t)w1[1] << 32), h1 = w1[2] | ((uint64_t)w1[3] << 32);
             if (s == 0) {
               if (act0 && !def0) store_dense(vals, r0, l0, h0);
               if (act1 && !def1) store_dense(vals, r1, l1, h1);

@@ -77,3 +77,19 @@ def test_config_errors():
         P.plan_update(P.ReplicatorConfig(P.Scheme.Random, compression=1e-6), 100, 0, 0)
     with pytest.raises(P.ConfigError, match="stride period"):
         P.plan_update(P.ReplicatorConfig(P.Scheme.Striding, compression=0.25), 3, 0, 0)
+
+
+def test_sort16_network():
+    """The select warps' 16-input sorting network (demo_tc_adam.cu, DMB_SORT16_NET) sorts
+    every 0-1 input, hence every input (0-1 principle)."""
+    import numpy as np
+
+    src = open(os.path.join(ROOT, "paper_2502_06728_b200", "csrc", "demo_tc_adam.cu")).read()
+    body = src[src.index("#define DMB_SORT16_NET(X)"):src.index("__device__ __forceinline__ void sort16_desc")]
+    pairs = [(int(i), int(j)) for i, j in re.findall(r"X\((\d+), (\d+)\)", body)]
+    assert len(pairs) == 60
+    x = ((np.arange(1 << 16)[:, None] >> np.arange(16)) & 1).astype(np.int8)
+    for i, j in pairs:
+        hi, lo = np.maximum(x[:, i], x[:, j]), np.minimum(x[:, i], x[:, j])
+        x[:, i], x[:, j] = hi, lo
+    assert (np.diff(x, axis=1) <= 0).all()
