@@ -1197,15 +1197,22 @@ teardown:
 }
 
 // ---------------------------------------------------------------------------
-// FP64 fix-up of the full chunks the tensor-core kernel could not certify (fb_list): one
-// warp per chunk, lane j holds coefficients j and j+32.  The coefficients are re-derived
-// in the oracle's operation order (acc = 0; acc = acc + B[j][i]*x_i, ascending i, no FMA:
-// transform.cpp:56-63) from the FP64 basis in shared memory, the TopK is exact on them
-// (ties toward the lower index, transform.cpp:127-133), then the chunk gets the same wire
-// values, payload and W = wire - coef -> D = IDCT(W) -> AdamW as in the main kernel (whose
-// apply warps left this chunk's state untouched).
+// Fix-up of the full chunks the tensor-core kernel could not certify (fb_list): one warp
+// per chunk, lane j holds coefficients j and j+32.  First an FP32 pass: the coefficients
+// by eight FMA chains and a summation tree, whose error against the oracle's FP64 values is
+// rigorously below kFmaEps * ||x||_1 (gamma_11 + u for the rounded basis, times max|B| =
+// sqrt(2/64)) -- 13x tighter than the tensor-core kernel's 3xTF32 radius, so nearly every
+// deferred chunk settles here.  A chunk it cannot certify either is re-derived in FP64 in the oracle's operation
+// order (acc = 0; acc = acc + B[j][i]*x_i, ascending i, no FMA: transform.cpp:56-63) from
+// the FP64 basis in shared memory, and the TopK is exact on those values (ties toward the
+// lower index, transform.cpp:127-133).  Then the chunk gets the same wire values, payload
+// and W = wire - coef -> D = IDCT(W) -> AdamW as in the main kernel (whose apply warps left
+// this chunk's state untouched).
 constexpr int kFixWarps = 8;
-constexpr uint32_t FIX_SMEM = S * S * 8 + S * S * 4 + kFixWarps * S * 8;  // FP64 + FP32 basis, x per warp
+// B64 (swizzled), B row-major, B^T, then x per warp (FP64, or FP32 in the FMA pass)
+constexpr uint32_t FIX_SMEM = S * S * 8 + S * S * 4 + S * S * 4 + kFixWarps * S * 8;
+// gamma_11 of the chains and the tree plus u for the FP32 basis: 12 * 2^-24, with margin
+constexpr float kFmaEps = 14.0f * 5.9604645e-8f * 0.17677669f;
 
 template <ChunkMode MODE, int WIRE>
 __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkArgs a) {
@@ -1214,15 +1221,19 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
   extern __shared__ __align__(16) uint8_t fsm[];
   double* b64 = reinterpret_cast<double*>(fsm);       // (j, i) at j*64 + (i ^ (j & 15))
   float* b32 = reinterpret_cast<float*>(fsm + S * S * 8);  // B[j][i] row-major
-  double* xw = reinterpret_cast<double*>(fsm + S * S * 12) + (threadIdx.x >> 5) * S;  // this warp's chunk
+  float* bt = reinterpret_cast<float*>(fsm + S * S * 12);    // B^T: (i, j) at i*64 + j
+  double* xw = reinterpret_cast<double*>(fsm + S * S * 16) + (threadIdx.x >> 5) * S;  // this warp's chunk
+  float* xf = reinterpret_cast<float*>(xw);
   if (*a.fb_count == 0) return;
   if (!kEncodeOnly && step_failed(a.status)) return;
   for (int u = threadIdx.x; u < S * S; u += blockDim.x) {
     const int j = u >> 6, i = u & 63;
     b64[j * S + (i ^ (j & 15))] = a.basis.B64[u];
     b32[u] = a.basis.B[u];
+    bt[u] = a.basis.B[i * S + j];  // here u = i' * 64 + j' with i' = j, j' = i
   }
   __syncthreads();
+  const bool need_signs = a.geo.sign_mode || a.geo.dtype == DMB_TERNARY;
   const int lane = threadIdx.x & 31;
   const int k = a.geo.k;
   const bool full_band = k == S;
@@ -1230,6 +1241,7 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
   const bool sign_mode = a.geo.sign_mode;
   const uint64_t nvals = a.geo.nchunks * (uint64_t)k;
   const unsigned n = *a.fb_count;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.status) atomicAdd(&a.status->fallback_chunks, (unsigned long long)n);
   const unsigned nwarps = gridDim.x * kFixWarps;
   for (unsigned u = blockIdx.x * kFixWarps + (threadIdx.x >> 5); u < n; u += nwarps) {
     const uint64_t c = a.fb_list[u];
@@ -1239,12 +1251,86 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
       x0 = __fadd_rn(__fmul_rn(a.sgd.beta, a.m_in[g0 + lane]), x0);
       x1 = __fadd_rn(__fmul_rn(a.sgd.beta, a.m_in[g0 + lane + 32]), x1);
     }
+    bool sel0 = true, sel1 = true, settled = false;
+    float c0f = 0.0f, c1f = 0.0f, w0 = 0.0f, w1 = 0.0f;
+    __syncwarp();  // the previous chunk's reads of this warp's x buffer are done
+    if (!a.force_fp64) {
+      // ---- FP32 pass: FMA chains (two partial sums per coefficient) + certification ----
+      xf[lane] = x0;
+      xf[lane + 32] = x1;
+      __syncwarp();
+      // eight FMA chains of eight terms per coefficient, then a depth-3 tree: the rounding
+      // error is within gamma_11 of sum |b x| (gamma_64 for one chain)
+      float s0[8], s1[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s0[e] = s1[e] = 0.0f;
+      const float4* x4 = reinterpret_cast<const float4*>(xf);
+#pragma unroll
+      for (int q = 0; q < S / 4; ++q) {
+        const float4 v = x4[q];  // broadcast read
+        const float* r = bt + 4 * q * S;
+        const int e = (4 * q) & 7;
+        s0[e] = fmaf(r[lane], v.x, s0[e]);
+        s1[e] = fmaf(r[lane + 32], v.x, s1[e]);
+        s0[e + 1] = fmaf(r[S + lane], v.y, s0[e + 1]);
+        s1[e + 1] = fmaf(r[S + lane + 32], v.y, s1[e + 1]);
+        s0[e + 2] = fmaf(r[2 * S + lane], v.z, s0[e + 2]);
+        s1[e + 2] = fmaf(r[2 * S + lane + 32], v.z, s1[e + 2]);
+        s0[e + 3] = fmaf(r[3 * S + lane], v.w, s0[e + 3]);
+        s1[e + 3] = fmaf(r[3 * S + lane + 32], v.w, s1[e + 3]);
+      }
+      const float f0 = ((s0[0] + s0[1]) + (s0[2] + s0[3])) + ((s0[4] + s0[5]) + (s0[6] + s0[7]));
+      const float f1 = ((s1[0] + s1[1]) + (s1[2] + s1[3])) + ((s1[4] + s1[5]) + (s1[6] + s1[7]));
+      float l1 = fabsf(x0) + fabsf(x1);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) l1 += __shfl_xor_sync(kFull, l1, o);
+      const float eps = kFmaEps * l1;
+      const uint32_t q0 = __float_as_uint(fabsf(f0)), q1 = __float_as_uint(fabsf(f1));
+      bool ok = true, fs0 = true, fs1 = true;
+      if (!full_band) {  // the k-th largest key by MSB radix select; ties are left to FP64
+        const uint32_t mx = __reduce_max_sync(kFull, max(q0, q1)), mn = __reduce_min_sync(kFull, min(q0, q1));
+        const uint32_t diff = mx ^ mn;
+        const int top = diff ? 31 - __clz((int)diff) : -1;
+        uint32_t T = top >= 0 ? (mx & ~((2u << top) - 1u)) : mx;
+        ok = false;
+        for (int b = top; b >= 0; --b) {
+          const uint32_t cand = T | (1u << b);
+          const int cnt = __popc(__ballot_sync(kFull, q0 >= cand)) + __popc(__ballot_sync(kFull, q1 >= cand));
+          if (cnt >= k) {
+            T = cand;
+            if (cnt == k) {
+              ok = true;
+              break;
+            }
+          }
+        }
+        fs0 = q0 >= T;
+        fs1 = q1 >= T;
+        if (ok) {
+          const float kth = __uint_as_float(__reduce_min_sync(kFull, min(fs0 ? q0 : ~0u, fs1 ? q1 : ~0u)));
+          const float nxt = __uint_as_float(__reduce_max_sync(kFull, max(fs0 ? 0u : q0, fs1 ? 0u : q1)));
+          ok = kth - nxt > 2.0f * eps && (!need_signs || kth > eps);
+        }
+      } else if (need_signs) {
+        ok = __uint_as_float(__reduce_min_sync(kFull, min(q0, q1))) > eps;
+      }
+      if (ok) {  // warp-uniform
+        settled = true;
+        sel0 = fs0;
+        sel1 = fs1;
+        c0f = f0;
+        c1f = f1;
+        w0 = sel0 ? cond_w<WIRE>(f0) : 0.0f;
+        w1 = sel1 ? cond_w<WIRE>(f1) : 0.0f;
+      }
+      __syncwarp();  // x reads done before the FP64 pass reuses the buffer
+    }
+    if (!settled) {
     // exact coefficients
     double cd0 = 0.0, cd1 = 0.0;
     const double* r0 = b64 + lane * S;
     const double* r1 = b64 + (lane + 32) * S;
     const int sw = lane & 15;
-    __syncwarp();  // the previous chunk's reads of xw are done
     xw[lane] = (double)x0;
     xw[lane + 32] = (double)x1;
     __syncwarp();
@@ -1255,7 +1341,6 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
       cd1 = __dadd_rn(cd1, __dmul_rn(r1[i ^ sw], xi));
     }
     // exact TopK: MSB radix select on the |c| bit patterns from their common prefix
-    bool sel0 = true, sel1 = true;
     if (!full_band) {
       const uint64_t k0 = (uint64_t)__double_as_longlong(fabs(cd0)), k1 = (uint64_t)__double_as_longlong(fabs(cd1));
       uint64_t mx = k0 > k1 ? k0 : k1, mn = k0 < k1 ? k0 : k1;
@@ -1292,9 +1377,11 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
         sel1 = k1 > T || (k1 == T && __popc(e0) + __popc(e1 & lt) < need);
       }
     }
-    const float c0f = (float)cd0, c1f = (float)cd1;
-    const float w0 = sel0 ? condition_f64(cd0, dtype, sign_mode) : 0.0f;
-    const float w1 = sel1 ? condition_f64(cd1, dtype, sign_mode) : 0.0f;
+    c0f = (float)cd0;
+    c1f = (float)cd1;
+    w0 = sel0 ? condition_f64(cd0, dtype, sign_mode) : 0.0f;
+    w1 = sel1 ? condition_f64(cd1, dtype, sign_mode) : 0.0f;
+    }
     // payload: ascending frequency (MASK layout: u64 mask, then the values)
     if (a.body) {
       const unsigned m0 = __ballot_sync(kFull, sel0), m1 = __ballot_sync(kFull, sel1);
