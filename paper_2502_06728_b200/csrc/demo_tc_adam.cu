@@ -1,32 +1,36 @@
 // demo_tc_adam.cu -- warp-specialised tensor-core DeMo kernel for the decoupled-AdamW
 // paths at chunk size 64 (the bench headline: OLMo-1B-shaped FlexDeMo + AdamW on one B200).
 //
-// One persistent CTA per SM, tiles of 128 chunks (8192 parameters), three roles that
-// run concurrently on different tiles:
+// One persistent CTA per SM, tiles of 128 chunks (8192 parameters), 14 warps in four roles
+// that run concurrently on different tiles:
 //   select warps 0-7  (quad layout, tcgen05.ld/st 16x256b: 4 lanes per chunk, 2 chunks
 //                      per quad, column 8r + 2(lane%4) + b)
-//        - gradient tile t+1 (TMA, 128B swizzle) -> TF32 hi/lo + raw copy -> TMEM,
-//          ||x||_1 per chunk, require_finite
-//        - coefficients of tile t from TMEM -> TopK (radix select), certification against
-//          the FP64 oracle, exact FP64 re-derivation of what the FP32 bound cannot order,
-//          payload, W = wire - coef on the selection -> TMEM (TF32 hi/lo)
-//   apply warps 8-15  (slice layout, tcgen05.ld 32x32b: thread = chunk, 32 columns)
+//        - coefficients of tile t from TMEM -> TopK (bitonic threshold for k = 8/16/32 of
+//          64, radix select otherwise), certification of order and signs against the FP64
+//          oracle (an uncertified chunk goes to the fix-up kernel), payload, W = wire - coef
+//          on the selection -> TMEM (TF32 hi/lo); in merge mode the R gathered payloads
+//   apply warps 8-11  (slice layout, tcgen05.ld 32x32b: thread = chunk row)
 //        - D = IDCT(W) and the raw gradient from TMEM, p / exp_avg / exp_avg_sq from the
-//          shared-memory staging tile (TMA), decoupled AdamW in place in the staging tile
-//   control warp 16   - every TMA load / store and every tcgen05.mma, in tile order:
-//                       forward C = X B^T and inverse D = W B in 3xTF32 (A from TMEM)
+//          shared-memory staging tile (TMA), decoupled AdamW (or SGD) in place there
+//        - then the front of tile t+2: gradient tile (TMA, 128B swizzle) -> TF32 hi/lo +
+//          raw copy -> TMEM, ||x||_1 per chunk, require_finite
+//   MMA warp 12       - gradient TMA and every tcgen05.mma, in tile order: forward
+//                       C = X B^T and inverse D = W B in 3xTF32 (A from TMEM)
+//   state warp 13     - optimizer-state TMA loads / stores (two 32-column halves)
 // The optimizer state streams through shared memory with TMA bulk tensor copies, so the
 // HBM traffic of tile t overlaps the selection of tile t+1 without occupying registers.
+// Every hand-off is an mbarrier; control warps stay converged (lane 0 issues).
 //
-// TMEM columns: C [0,64)  D [64,128)  X/W hi [128,192)  X/W lo [192,256)  raw gradient
-// ring of three tiles [256,448).  W reuses the X columns (X of t+1 is consumed by the
-// forward MMA before W of t is written; W of t by the inverse before X of t+2).
+// TMEM columns (AdamW): C [0,64)  D [64,128)  X/W hi [128,192)  X/W lo [192,256)  raw
+// gradient ring of three tiles [256,448); SGD keeps a second W and D there instead.  W
+// reuses the X columns (X of t+1 is consumed by the forward MMA before W of t is written;
+// W of t by the inverse before X of t+2).
 //
 // Reference: transform.cpp:56-73, :127-147 (DCT, TopK, inverse); replicate.cpp:137-144,
 // :282-309 (conditioning, merge); optim.cpp:51-74 (decoupled AdamW).  Modes: StepAdam
 // (prepare + merge(R=1) + apply), MergeAdam (R gathered payloads + own indices -> apply),
-// EncodeAdam (payload only).  The one partial chunk at the shard end is handed to the
-// SIMT kernel through the fallback list.
+// EncodeAdam (payload only), StepSgd.  The one partial chunk at the shard end is handed to
+// the SIMT kernel; uncertified chunks to demo_fix64_kernel, which runs right after.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -1015,7 +1019,14 @@ __global__ void __maxnreg__(128)
               asm volatile("cp.async.wait_group 0;" ::: "memory");
               __syncwarp();
             }
+            // the member sum of codes is an integer per column: count it bit-parallel.  Per
+            // 32-bit half-word of codes, each of its two 16-bit lanes (r & 1) accumulates
+            // plus + (1 - minus) for the even (b = 0) and the odd (b = 1) column of the
+            // thread, i.e. value + 1 per member; the values are exact in FP32 whatever the order
             const int q = lane >> 2;
+            constexpr uint32_t M = 0x00010001u;
+            uint32_t ce[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, co[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            const int s4 = 4 * s;
             for (int rr = 0; rr < a.in.R; ++rr) {
               uint64_t lo0, hi0, lo1, hi1;
               if (staged) {
@@ -1030,13 +1041,21 @@ __global__ void __maxnreg__(128)
                 lo1 = act1 ? __ldg(dv + 2 * r1) : 0ull;
                 hi1 = act1 ? __ldg(dv + 2 * r1 + 1) : 0ull;
               }
-              const uint64_t a0 = lo0 >> (4 * s), b0 = hi0 >> (4 * s), a1 = lo1 >> (4 * s), b1 = hi1 >> (4 * s);
+              const uint32_t w[8] = {(uint32_t)lo0, (uint32_t)(lo0 >> 32), (uint32_t)hi0, (uint32_t)(hi0 >> 32),
+                                     (uint32_t)lo1, (uint32_t)(lo1 >> 32), (uint32_t)hi1, (uint32_t)(hi1 >> 32)};
 #pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                const int r = e >> 1, sh = 16 * (r & 3) + 2 * (e & 1);
-                gq0[e] += value_of((uint32_t)((r < 4 ? a0 : b0) >> sh) & 3u);
-                gq1[e] += value_of((uint32_t)((r < 4 ? a1 : b1) >> sh) & 3u);
+              for (int i = 0; i < 8; ++i) {
+                ce[i] += ((w[i] >> s4) & M) + (~(w[i] >> (s4 + 1)) & M);
+                co[i] += ((w[i] >> (s4 + 2)) & M) + (~(w[i] >> (s4 + 3)) & M);
               }
+            }
+            const int Rm = a.in.R;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {  // element e = 2r + b: half-word r / 2, lane r & 1
+              const int r = e >> 1, i = r >> 1, sh = 16 * (r & 1);
+              const uint32_t* c = (e & 1) ? co : ce;
+              gq0[e] = act0 ? (float)((int)((c[i] >> sh) & 0xffffu) - Rm) : 0.0f;
+              gq1[e] = act1 ? (float)((int)((c[4 + i] >> sh) & 0xffffu) - Rm) : 0.0f;
             }
             if (staged) __syncwarp();  // the scratch is rewritten by the next tile
             sel0 = act0 ? gather16(om0, s) : 0u;

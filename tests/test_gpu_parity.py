@@ -502,14 +502,16 @@ def test_tc_fused_step_matches_oracle(oracle, monkeypatch, opt_kind, force):
     assert np.array_equal(idx, want["freq_indices"])
 
 
-@pytest.mark.parametrize("k,force,wire,sign", [(32, False, 0, True), (8, False, 0, True), (32, True, 0, True),
-                                               (32, False, 1, True), (8, True, 1, True), (16, False, 1, False)])
-def test_tc_cluster_adamw_prepare_merge_matches_oracle(oracle, monkeypatch, k, force, wire, sign):
+@pytest.mark.parametrize("k,force,wire,sign,R", [(32, False, 0, True, 3), (8, False, 0, True, 3), (32, True, 0, True, 3),
+                                                 (32, False, 1, True, 3), (8, True, 1, True, 3), (16, False, 1, False, 3),
+                                                 (32, False, 1, True, 8), (16, False, 1, True, 17)])
+def test_tc_cluster_adamw_prepare_merge_matches_oracle(oracle, monkeypatch, k, force, wire, sign, R):
     """The N>1 path as cluster.py drives it: dmb_adamw_prepare (no local_q: the tensor-core
     encode kernel) on R members' gradients, then dmb_merge_apply_adamw of the R bodies for one
     member (the tensor-core merge kernel) -- payloads and state against the oracle's
     select_and_encode / decode_and_merge / adamw_apply (cluster.cpp:193-231).  wire=1: the
-    MASK exchange layout, whose serialize() must still be the reference's bytes."""
+    MASK exchange layout, whose serialize() must still be the reference's bytes; R = 17 takes
+    the merge's unstaged path (more members than the scratch holds)."""
     import ctypes as C
 
     from paper_2502_06728_b200 import _capi
@@ -521,8 +523,8 @@ def test_tc_cluster_adamw_prepare_merge_matches_oracle(oracle, monkeypatch, k, f
         monkeypatch.setenv("DMB_FORCE_FP64", "1")
     lib = _capi.lib
     n = 64 * 128 * 6 + 64 * 3 + (0 if wire else 7)  # partial last tile (and chunk: reference layout)
-    R, own, step, lr = 3, 1, 5, 0.002
-    rng = np.random.default_rng(31 + k)
+    own, step, lr = 1, 5, 0.002
+    rng = np.random.default_rng(31 + k + R)
     gs = [(rng.standard_normal(n) * 1e-3).astype(np.float32) for _ in range(R)]
     rep = Rep(scheme=DEMO, chunk_size=64, top_k=k, compression=k / 64, sign_mode=sign, seed=1234)
     c = rep_to_cfg(rep).c()
