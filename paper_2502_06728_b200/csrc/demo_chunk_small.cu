@@ -24,7 +24,9 @@ void launch_chunk_kernel(ChunkMode mode, const ChunkArgs& a_in, cudaStream_t str
     // warp-specialised tensor-core kernel; the chunks its FP32 bound cannot certify are
     // re-derived exactly by the FP64 fix-up kernel; a partial last chunk (its own
     // length and basis) goes through the SIMT kernel
-    cudaMemsetAsync(a.fb_count, 0, sizeof(unsigned), stream);
+    // a merge never defers: it leaves the fix-up list to an encode that may be running
+    // concurrently on another stream
+    if (mode != ChunkMode::MergeAdam) cudaMemsetAsync(a.fb_count, 0, sizeof(unsigned), stream);
     timer_begin(stream);
     launch_tc3_kernel(mode, a, stream);
     timer_end(stream);
