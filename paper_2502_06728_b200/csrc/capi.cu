@@ -101,7 +101,7 @@ std::vector<double> host_basis(int s) {
 struct BasisBuf {
   float* B = nullptr;
   float* BT = nullptr;
-  double* B64 = nullptr;
+  double* B64 = nullptr;  // B64 | B64T, each s*s
   float* tf32 = nullptr;  // Bhi | Blo | BThi | BTlo, each s*s
 };
 
@@ -168,7 +168,11 @@ int get_basis(dmb_ctx* ctx, int s, Basis* out) {
     DMB_CUDA_TRY(cudaMemcpy(buf.tf32, split.data(), split.size() * sizeof(float), cudaMemcpyHostToDevice));
     DMB_CUDA_TRY(cudaMalloc(&buf.B, b.size() * sizeof(float)));
     DMB_CUDA_TRY(cudaMalloc(&buf.BT, bt.size() * sizeof(float)));
-    DMB_CUDA_TRY(cudaMalloc(&buf.B64, b64.size() * sizeof(double)));
+    DMB_CUDA_TRY(cudaMalloc(&buf.B64, 2 * b64.size() * sizeof(double)));
+    std::vector<double> b64t((size_t)s * s);
+    for (int j = 0; j < s; ++j)
+      for (int i = 0; i < s; ++i) b64t[(size_t)i * s + j] = b64[(size_t)j * s + i];
+    DMB_CUDA_TRY(cudaMemcpy(buf.B64 + b64.size(), b64t.data(), b64t.size() * sizeof(double), cudaMemcpyHostToDevice));
     DMB_CUDA_TRY(cudaMemcpy(buf.B, b.data(), b.size() * sizeof(float), cudaMemcpyHostToDevice));
     DMB_CUDA_TRY(cudaMemcpy(buf.BT, bt.data(), bt.size() * sizeof(float), cudaMemcpyHostToDevice));
     DMB_CUDA_TRY(cudaMemcpy(buf.B64, b64.data(), b64.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -179,6 +183,7 @@ int get_basis(dmb_ctx* ctx, int s, Basis* out) {
   out->BT = it->second.BT;
   out->B64 = it->second.B64;
   const size_t ss = (size_t)s * s;
+  out->B64T = it->second.B64 + ss;
   out->Bhi = it->second.tf32;
   out->Blo = it->second.tf32 + ss;
   out->BThi = it->second.tf32 + 2 * ss;

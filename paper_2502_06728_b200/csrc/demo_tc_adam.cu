@@ -1223,13 +1223,14 @@ teardown:
 // sqrt(2/64)) -- 13x tighter than the tensor-core kernel's 3xTF32 radius, so nearly every
 // deferred chunk settles here.  A chunk it cannot certify either is re-derived in FP64 in the oracle's operation
 // order (acc = 0; acc = acc + B[j][i]*x_i, ascending i, no FMA: transform.cpp:56-63) from
-// the FP64 basis in shared memory, and the TopK is exact on those values (ties toward the
+// the FP64 basis, and the TopK is exact on those values (ties toward the
 // lower index, transform.cpp:127-133).  Then the chunk gets the same wire values, payload
 // and W = wire - coef -> D = IDCT(W) -> AdamW as in the main kernel (whose apply warps left
 // this chunk's state untouched).
 constexpr int kFixWarps = 8;
-// B64 (swizzled), B row-major, B^T, then x per warp (FP64, or FP32 in the FMA pass)
-constexpr uint32_t FIX_SMEM = S * S * 8 + S * S * 4 + S * S * 4 + kFixWarps * S * 8;
+// B row-major, B^T, then x per warp (FP64, or FP32 in the FMA pass); the rare FP64 pass
+// reads the FP64 basis through L1
+constexpr uint32_t FIX_SMEM = S * S * 4 + S * S * 4 + kFixWarps * S * 8;
 // gamma_11 of the chains and the tree plus u for the FP32 basis: 12 * 2^-24, with margin
 constexpr float kFmaEps = 14.0f * 5.9604645e-8f * 0.17677669f;
 
@@ -1238,18 +1239,15 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
   constexpr bool kEncodeOnly = MODE == ChunkMode::EncodeAdam;
   constexpr bool kSgd = MODE == ChunkMode::StepSgd;
   extern __shared__ __align__(16) uint8_t fsm[];
-  double* b64 = reinterpret_cast<double*>(fsm);       // (j, i) at j*64 + (i ^ (j & 15))
-  float* b32 = reinterpret_cast<float*>(fsm + S * S * 8);  // B[j][i] row-major
-  float* bt = reinterpret_cast<float*>(fsm + S * S * 12);    // B^T: (i, j) at i*64 + j
-  double* xw = reinterpret_cast<double*>(fsm + S * S * 16) + (threadIdx.x >> 5) * S;  // this warp's chunk
+  float* b32 = reinterpret_cast<float*>(fsm);              // B[j][i] row-major
+  float* bt = reinterpret_cast<float*>(fsm + S * S * 4);    // B^T: (i, j) at i*64 + j
+  double* xw = reinterpret_cast<double*>(fsm + S * S * 8) + (threadIdx.x >> 5) * S;  // this warp's chunk
   float* xf = reinterpret_cast<float*>(xw);
   if (*a.fb_count == 0) return;
   if (!kEncodeOnly && step_failed(a.status)) return;
-  for (int u = threadIdx.x; u < S * S; u += blockDim.x) {
-    const int j = u >> 6, i = u & 63;
-    b64[j * S + (i ^ (j & 15))] = a.basis.B64[u];
-    b32[u] = a.basis.B[u];
-    bt[u] = a.basis.B[i * S + j];  // here u = i' * 64 + j' with i' = j, j' = i
+  for (int u = 4 * threadIdx.x; u < S * S; u += 4 * blockDim.x) {
+    *reinterpret_cast<float4*>(b32 + u) = __ldg(reinterpret_cast<const float4*>(a.basis.B + u));
+    *reinterpret_cast<float4*>(bt + u) = __ldg(reinterpret_cast<const float4*>(a.basis.BT + u));
   }
   __syncthreads();
   const bool need_signs = a.geo.sign_mode || a.geo.dtype == DMB_TERNARY;
@@ -1347,17 +1345,15 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
     if (!settled) {
     // exact coefficients
     double cd0 = 0.0, cd1 = 0.0;
-    const double* r0 = b64 + lane * S;
-    const double* r1 = b64 + (lane + 32) * S;
-    const int sw = lane & 15;
+    const double* bt64 = a.basis.B64T + lane;  // B[lane][i] at i*64 + lane: coalesced, L1-resident
     xw[lane] = (double)x0;
     xw[lane + 32] = (double)x1;
     __syncwarp();
 #pragma unroll 8
     for (int i = 0; i < S; ++i) {
       const double xi = xw[i];  // broadcast read
-      cd0 = __dadd_rn(cd0, __dmul_rn(r0[i ^ sw], xi));
-      cd1 = __dadd_rn(cd1, __dmul_rn(r1[i ^ sw], xi));
+      cd0 = __dadd_rn(cd0, __dmul_rn(__ldg(bt64 + i * S), xi));
+      cd1 = __dadd_rn(cd1, __dmul_rn(__ldg(bt64 + i * S + 32), xi));
     }
     // exact TopK: MSB radix select on the |c| bit patterns from their common prefix
     if (!full_band) {

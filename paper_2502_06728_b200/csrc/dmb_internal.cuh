@@ -125,6 +125,7 @@ struct Basis {
   const float* B;    // [j][i] row-major, s*s
   const float* BT;   // [i][j] transposed
   const double* B64; // [j][i] row-major
+  const double* B64T; // [i][j] transposed
   // TF32 splits for the tensor-core path (hi = RNA_tf32(B64), lo = RNA_tf32(B64 - hi))
   const float* Bhi;
   const float* Blo;
