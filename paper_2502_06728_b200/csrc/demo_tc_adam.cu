@@ -1157,17 +1157,29 @@ __global__ void __maxnreg__(128)
             const float x1 = full_band || on1 ? cond_w<WIRE>(c1[e]) : 0.0f;
             u0[e] = def0 ? __int_as_float(0x7fc00000) : (act0 ? x0 : 0.0f);
             u1[e] = def1 ? __int_as_float(0x7fc00000) : (act1 ? x1 : 0.0f);
-          } else if (kMerge) {
+          } else if (kMerge) {  // an inactive row has no selection and an empty grid row
             const float g0v = a.geo.wire_mask ? gq0[e] : grid[l0 * S + (col ^ ((l0 & 7) << 3))];
             const float g1v = a.geo.wire_mask ? gq1[e] : grid[l1 * S + (col ^ ((l1 & 7) << 3))];
             v0 = g0v * invR - ((on0 && !full_band) ? c0[e] : 0.0f);
             v1 = g1v * invR - ((on1 && !full_band) ? c1[e] : 0.0f);
+          } else if (WIRE == kWireSign) {
+            // the selection is empty on an inactive row; on a stored (certified) row every
+            // selected |c| is above the radius, so cond(c) = copysign(1, c) there
+            v0 = on0 ? copysignf(1.0f, c0[e]) - (full_band ? 0.0f : c0[e]) : 0.0f;
+            v1 = on1 ? copysignf(1.0f, c1[e]) - (full_band ? 0.0f : c1[e]) : 0.0f;
           } else {
-            v0 = full_band ? cond_w<WIRE>(c0[e]) : (on0 ? cond_w<WIRE>(c0[e]) - c0[e] : 0.0f);
-            v1 = full_band ? cond_w<WIRE>(c1[e]) : (on1 ? cond_w<WIRE>(c1[e]) - c1[e] : 0.0f);
+            v0 = on0 ? cond_w<WIRE>(c0[e]) - (full_band ? 0.0f : c0[e]) : 0.0f;
+            v1 = on1 ? cond_w<WIRE>(c1[e]) - (full_band ? 0.0f : c1[e]) : 0.0f;
           }
-          w0[e] = def0 ? __int_as_float(0x7fc00000) : (act0 ? v0 : 0.0f);
-          w1[e] = def1 ? __int_as_float(0x7fc00000) : (act1 ? v1 : 0.0f);
+          w0[e] = v0;
+          w1[e] = v1;
+        }
+        if (__any_sync(kFull, def0 || def1)) {  // rare: NaN-tag the deferred rows
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            if (def0) w0[e] = __int_as_float(0x7fc00000);
+            if (def1) w1[e] = __int_as_float(0x7fc00000);
+          }
         }
         evt(a, tid == 0, it, 7);
         if (has_next) mbar_wait(bar_f, (it + 1) & 1);  // X of t+1 consumed: the columns take W
