@@ -291,6 +291,16 @@ __device__ __forceinline__ uint32_t row_finish(const RowSel& r, const float (&c)
 // ---- bitonic TopK threshold (k = 8, 16, 32 of 64): the k-th largest |c| of a chunk held
 // by a quad (16 values per lane) from a local bitonic sort and merge-max steps across the
 // quad -- no data-dependent loop, every step independent compare-exchanges ----
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 __device__ __forceinline__ void cas_desc(float& x, float& y) {
   const float hi = fmaxf(x, y);
   y = fminf(x, y);
@@ -347,9 +357,9 @@ __device__ __forceinline__ float kth_bitonic(const float (&c)[16], int k, float&
     for (int i = 0; i < 16; ++i) p[i] = __shfl_sync(kFull, a[15 - i], lane ^ 3);
     float n = 0.0f;  // the bottom 32 of the same merge: its maximum is the 33rd largest
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      m = fminf(m, fmaxf(a[i], p[i]));
-      n = fmaxf(n, fminf(a[i], p[i]));
+    for (int i = 0; i < 16; i += 2) {  // three-input min / max (FMNMX3)
+      m = fmin3(m, fmaxf(a[i], p[i]), fmaxf(a[i + 1], p[i + 1]));
+      n = fmax3(n, fminf(a[i], p[i]), fminf(a[i + 1], p[i + 1]));
     }
     m = fminf(m, __shfl_xor_sync(kFull, m, 1));
     nxt = fmaxf(n, __shfl_xor_sync(kFull, n, 1));
@@ -362,7 +372,7 @@ __device__ __forceinline__ float kth_bitonic(const float (&c)[16], int k, float&
 #pragma unroll
     for (int i = 0; i < 16; ++i) p[i] = __shfl_sync(kFull, a[15 - i], lane ^ 2);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) m = fminf(m, fmaxf(a[i], p[i]));
+    for (int i = 0; i < 16; i += 2) m = fmin3(m, fmaxf(a[i], p[i]), fmaxf(a[i + 1], p[i + 1]));
   } else {  // k == 8
 #pragma unroll
     for (int i = 0; i < 8; ++i) p[i] = __shfl_sync(kFull, a[7 - i], lane ^ 1);
@@ -372,7 +382,7 @@ __device__ __forceinline__ float kth_bitonic(const float (&c)[16], int k, float&
 #pragma unroll
     for (int i = 0; i < 8; ++i) p[i] = __shfl_sync(kFull, a[7 - i], lane ^ 2);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) m = fminf(m, fmaxf(a[i], p[i]));
+    for (int i = 0; i < 8; i += 2) m = fmin3(m, fmaxf(a[i], p[i]), fmaxf(a[i + 1], p[i + 1]));
   }
   return m;
 }
