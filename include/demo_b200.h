@@ -201,7 +201,8 @@ int dmb_require_finite(dmb_ctx* ctx, const float* v, uint64_t n, void* stream);
 /* synchronizes `stream`; DMB_TRAINING with *first_bad set if a non-finite gradient was
  * seen since the last call (the latch is then cleared), else DMB_OK */
 int dmb_status(dmb_ctx* ctx, void* stream, int64_t* first_bad);
-/* chunks whose FP32 TopK could not be certified and were recomputed in FP64 (cumulative) */
+/* chunks whose first TopK could not be certified and were re-derived by a fix-up pass
+ * (tighter FP32 bound, else FP64 in the oracle's order), cumulative */
 int dmb_fallback_chunks(dmb_ctx* ctx, void* stream, uint64_t* count);
 /* kernels launched by this context since creation (host counter) */
 uint64_t dmb_launch_count(dmb_ctx* ctx);
