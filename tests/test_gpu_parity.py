@@ -575,3 +575,59 @@ def test_tc_cluster_adamw_prepare_merge_matches_oracle(oracle, monkeypatch, k, f
     chunk_close(host(ead), ew, 64, tol=1e-4, what="exp_avg")
     chunk_close(host(esd), sw, 64, tol=1e-4, what="exp_avg_sq")
     update_close(host(pd), pw, p0, lr, 64)
+
+
+@pytest.mark.parametrize("sign,dtype", [(True, FP32), (False, FP32), (False, FP16)])
+def test_tc_near_ties_settle_in_fixup(oracle, monkeypatch, sign, dtype):
+    """Chunks built with the k-th and (k+1)-th |c| a relative 1e-3 .. 1e-7 apart: the
+    tensor-core kernel defers the close ones, the fix-up settles them with its FP32 FMA
+    tree or, closer still, in FP64 in the oracle's order -- indices bit-exact and the
+    AdamW state within tolerance either way (demo_tc_adam.cu, demo_fix64_kernel)."""
+    import ctypes as C
+
+    from paper_2502_06728_b200 import _capi
+    from paper_2502_06728_b200.core import _ptr, _stream, context
+
+    p = P()
+    monkeypatch.setenv("DMB_TC", "1")
+    S, k, nch = 64, 32, 128 * 6
+    rng = np.random.default_rng(77)
+    j = np.arange(S)
+    B = np.sqrt(2.0 / S) * np.cos(np.pi * (2 * j[None, :] + 1) * j[:, None] / (2 * S))
+    B[0] /= np.sqrt(2.0)
+    c = rng.standard_normal((nch, S)) * 1e-3
+    gaps = np.array([1e-3, 1e-4, 3e-5, 1e-7])[np.arange(nch) % 4]
+    for r in range(nch):
+        order = np.argsort(-np.abs(c[r]))
+        kth, nxt = order[k - 1], order[k]
+        c[r, nxt] = np.sign(c[r, nxt]) * abs(c[r, kth]) * (1.0 - gaps[r])
+    g = (c @ B).astype(np.float32).reshape(-1)  # x = B^T c per chunk
+    n = g.size
+    p0 = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    ea0 = (rng.standard_normal(n) * 0.05).astype(np.float32)
+    es0 = (ea0.astype(np.float64) ** 2 * 4 + 1e-4).astype(np.float32)
+    rep = Rep(scheme=DEMO, chunk_size=S, top_k=k, compression=0.5, sign_mode=sign, transfer_dtype=dtype, seed=1234)
+    cfg = rep_to_cfg(rep).c()
+    body = torch.empty(int(_capi.lib.dmb_update_capacity(C.byref(cfg), n)), dtype=torch.uint8, device="cuda")
+    hdr = _capi.Update()
+    hdr.body = body.data_ptr()
+    gd, pd, ead, esd = dev(g), dev(p0), dev(ea0), dev(es0)
+    o = p.OptimizerConfig(p.OptimizerKind.DecoupledAdamW).c()
+    steps = C.c_uint64(4)
+    before = p.fallback_chunks()
+    lr = 0.01
+    rc = _capi.lib.dmb_step_adamw_local(context().h, _ptr(gd), _ptr(pd), _ptr(pd), _ptr(ead), _ptr(ead), _ptr(esd),
+                                        _ptr(esd), C.byref(steps), n, C.byref(o), C.byref(cfg), 3, 0, lr,
+                                        C.byref(hdr), _stream())
+    assert rc == 0, _capi.lib.dmb_last_error()
+    p.status()
+    assert p.fallback_chunks() - before >= nch // 4, "the close chunks were not deferred"
+    want = oracle.select_and_encode(g.astype(np.float64), rep, 3, 0)
+    idx = body[: 4 * want["freq_indices"].size].view(torch.int32).cpu().numpy().astype(np.uint32)
+    assert np.array_equal(idx, want["freq_indices"])
+    q = oracle.decode_and_merge(rep, [want["values"]], [want["freq_indices"]], n, 3, 0)
+    pw, ew, sw = p0.astype(np.float64), ea0.astype(np.float64), es0.astype(np.float64)
+    oracle.adamw_apply(pw, ew, sw, 4, g.astype(np.float64), want["local_q"], q, 0.9, 0.999, 1e-8, 0.0, lr)
+    chunk_close(host(ead), ew, 64, tol=1e-4, what="exp_avg")
+    chunk_close(host(esd), sw, 64, tol=1e-4, what="exp_avg_sq")
+    update_close(host(pd), pw, p0, lr, 64)
