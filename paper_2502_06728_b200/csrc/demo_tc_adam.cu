@@ -659,7 +659,7 @@ __global__ void __maxnreg__(128)
         }
 #pragma unroll
         for (int e = 0; e < 16; ++e) l1 += fabsf(x[e]);
-        if (!kSgd) tmem_st16(tmem + tl + COL_G + 64 * (n % 3) + 16 * h, x);
+        if (!kSgd && !kEncodeOnly) tmem_st16(tmem + tl + COL_G + 64 * (n % 3) + 16 * h, x);  // raw g for the apply
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           hi[e] = tf32_hi(x[e]);
