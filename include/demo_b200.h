@@ -209,10 +209,23 @@ uint64_t dmb_launch_count(dmb_ctx* ctx);
 /* DeMo exchange format of the updates this context encodes (DMB_WIRE_REFERENCE default;
  * DMB_WIRE_MASK selects MASK, recorded as DMB_WIRE_MASK_SIGN in updates whose values are
  * signs).
- * DMB_WIRE_MASK applies where the tensor-core AdamW path runs (s = 64, whole chunks, no
- * local_q output); elsewhere the encoder keeps the reference layout.  Merges read each
- * update's wire_format. */
+ * DMB_WIRE_MASK applies to DeMo vectors of whole chunks at s = 64 (the tensor-core encoders
+ * of both optimizers); other vectors keep the reference layout (dmb_plan_exchange tells
+ * which).  Merges read each update's wire_format. */
 int dmb_set_wire_format(dmb_ctx* ctx, int32_t format);
+/* dmb_plan_update for this context: the header (wire_format, body bytes) the encoder will
+ * produce at this context's wire format, so a caller can size exchange slots before any
+ * prepare runs (the layout is decided from the configuration alone; a prepare that cannot
+ * honour it -- misaligned vectors, a local_q / m_accum output -- fails with DMB_CONFIG) */
+int dmb_plan_exchange(dmb_ctx* ctx, const dmb_rep_cfg* cfg, uint64_t len, uint64_t step, uint32_t shard,
+                      dmb_update* out);
+/* cross-rank step agreement (cluster.cpp:182: every gradient is checked before any state
+ * changes): export writes 1 to the device int *d_flag when this context's status latch is
+ * set, 0 otherwise; after the flags are max-reduced over the group (NCCL, on the device),
+ * import latches the context when the group flag is set, so every later kernel of the step
+ * is a no-op on every rank (dmb_status then reports DMB_TRAINING, first_bad = -2) */
+int dmb_latch_export(dmb_ctx* ctx, int32_t* d_flag, void* stream);
+int dmb_latch_import(dmb_ctx* ctx, const int32_t* d_flag, void* stream);
 /* instrumentation: when enabled, CUDA events bracket every launch of the dominant
  * tensor-core step kernel on its stream; read returns their summed time and count
  * (synchronizing on the recorded events) and clears them */

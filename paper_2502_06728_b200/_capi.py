@@ -98,6 +98,9 @@ _SIGS = {
     "dmb_fallback_chunks": (C.c_int, [P, P, PU64]),
     "dmb_launch_count": (U64, [P]),
     "dmb_set_wire_format": (C.c_int, [P, C.c_int32]),
+    "dmb_plan_exchange": (C.c_int, [P, PCFG, U64, U64, U32, PUPD]),
+    "dmb_latch_export": (C.c_int, [P, P, P]),
+    "dmb_latch_import": (C.c_int, [P, P, P]),
     "dmb_kernel_timer_enable": (C.c_int, [C.c_int]),
     "dmb_kernel_timer_read": (C.c_int, [C.POINTER(C.c_double), PU64]),
 }

@@ -52,6 +52,15 @@ void timer_end(cudaStream_t stream) {
 }
 }  // namespace dmb
 
+namespace dmb {
+__global__ void latch_export_kernel(const DevStatus* st, int32_t* flag) {
+  *flag = st->first_bad != kNoBad ? 1 : 0;
+}
+__global__ void latch_import_kernel(DevStatus* st, const int32_t* flag) {
+  if (*flag && st->first_bad == kNoBad) st->first_bad = kNoBad - 1ull;  // kPeerBad
+}
+}  // namespace dmb
+
 using namespace dmb;
 
 namespace {
@@ -501,6 +510,19 @@ int check_aux_protocol(dmb_ctx* ctx, cudaStream_t st) {
   return DMB_OK;
 }
 
+// The DeMo exchange layout this context emits for a vector of `len`: MASK wherever the
+// tensor-core encoder can run (s = 64, whole chunks, tensor maps available), decided from the
+// configuration alone so a caller can size its exchange slots with dmb_plan_exchange; the
+// encoder then fails loudly instead of changing layout (e.g. for misaligned vectors).
+bool mask_layout(const dmb_ctx* ctx, const dmb_rep_cfg* cfg, uint64_t len) {
+  return ctx->wire_format != DMB_WIRE_REFERENCE && cfg->scheme == DMB_DEMO && cfg->chunk_size == 64 && len >= 64 &&
+         len % 64 == 0 && tc_enabled() && tc3_available();
+}
+void set_mask_header(const dmb_rep_cfg* cfg, dmb_update* out) {
+  out->wire_format = (cfg->sign_mode || cfg->transfer_dtype == DMB_TERNARY) ? DMB_WIRE_MASK_SIGN : DMB_WIRE_MASK;
+  out->bytes = mask_body_bytes(out, cfg->transfer_dtype);
+}
+
 // Encode one vector (v = g, or m_acc from beta*m_in + g when sgd) into *out.
 int encode(dmb_ctx* ctx, DevStatus* st, bool sgd, const float* g, const float* m_in, float* m_out,
            double beta, uint64_t len, const dmb_rep_cfg* cfg, uint64_t step, uint32_t shard,
@@ -522,10 +544,11 @@ int encode(dmb_ctx* ctx, DevStatus* st, bool sgd, const float* g, const float* m
     a.sgd = sgd_scalars(beta, 0.0);
     a.status = st;
     if (int rc = attach_fallback(ctx, &a)) return rc;
-    if (ctx->wire_format != DMB_WIRE_REFERENCE && !sgd && len % cfg->chunk_size == 0 && tc_enabled() &&
-        tc3_supported(ChunkMode::EncodeAdam, a)) {
-      out->wire_format = (cfg->sign_mode || cfg->transfer_dtype == DMB_TERNARY) ? DMB_WIRE_MASK_SIGN : DMB_WIRE_MASK;
-      out->bytes = mask_body_bytes(out, cfg->transfer_dtype);
+    if (mask_layout(ctx, cfg, len)) {
+      if (!tc3_supported(sgd ? ChunkMode::EncodeSgd : ChunkMode::EncodeAdam, a))
+        return fail(DMB_CONFIG, "the MASK exchange layout needs the tensor-core encoder: 16-byte aligned vectors%s "
+                    "and no local_q / m_accum output", sgd ? " (distinct momentum buffers allowed)" : "");
+      set_mask_header(cfg, out);
       a.geo.wire_mask = 1;
     }
     if (int rc = prep_values_region(out, cfg->transfer_dtype, s)) return rc;
@@ -542,6 +565,9 @@ int encode(dmb_ctx* ctx, DevStatus* st, bool sgd, const float* g, const float* m
 }
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// first_bad of a step failed on another rank of the group (dmb_latch_import)
+constexpr unsigned long long kPeerBad = kNoBad - 1ull;
 
 }  // namespace
 
@@ -838,6 +864,12 @@ int dmb_merge_apply_sgd(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_upda
     a.p_out = params;
     a.sgd = sgd_scalars(0.0, lr);
     a.status = ctx->status;
+    if (int rc = attach_fallback(ctx, &a)) return rc;
+    if (is_mask(&updates[0])) {
+      if (!(len % cfg->chunk_size == 0 && tc_enabled() && tc3_supported(ChunkMode::MergeSgd, a)))
+        return fail(DMB_PROTOCOL, "mask-format updates need the tensor-core merge path (s = 64, whole chunks)");
+      a.geo.wire_mask = 1;
+    }
     launch_chunk_kernel(ChunkMode::MergeSgd, a, s);
     return last_launch();
   }
@@ -992,6 +1024,11 @@ int dmb_status(dmb_ctx* ctx, void* stream, int64_t* first_bad) {
     DMB_CUDA_TRY(cudaMemset(&ctx->status->protocol_error, 0, sizeof(unsigned int)));
     return fail(DMB_PROTOCOL, "frequency index out of range");
   }
+  if (h.first_bad == kPeerBad) {
+    DMB_CUDA_TRY(cudaMemset(&ctx->status->first_bad, 0xff, sizeof(unsigned long long)));
+    if (first_bad) *first_bad = -2;
+    return fail(DMB_TRAINING, "gradient contains a non-finite value (on another rank of the step)");
+  }
   if (h.first_bad != kNoBad) {
     DMB_CUDA_TRY(cudaMemset(&ctx->status->first_bad, 0xff, sizeof(unsigned long long)));
     return fail(DMB_TRAINING, "gradient contains a non-finite value (at index %llu)",
@@ -1034,6 +1071,28 @@ int dmb_kernel_timer_read(double* total_ms, uint64_t* launches) {
   if (total_ms) *total_ms = t;
   if (launches) *launches = n;
   return DMB_OK;
+}
+
+int dmb_plan_exchange(dmb_ctx* ctx, const dmb_rep_cfg* cfg, uint64_t len, uint64_t step, uint32_t shard,
+                      dmb_update* out) {
+  if (!ctx || !cfg || !out) return fail(DMB_CONFIG, "NULL argument");
+  if (int rc = plan(cfg, len, step, shard, out)) return rc;
+  if (!out->empty && mask_layout(ctx, cfg, len)) set_mask_header(cfg, out);
+  return DMB_OK;
+}
+
+int dmb_latch_export(dmb_ctx* ctx, int32_t* d_flag, void* stream) {
+  if (!ctx || !d_flag) return fail(DMB_CONFIG, "NULL argument");
+  latch_export_kernel<<<1, 1, 0, as_stream(stream)>>>(ctx->status, d_flag);
+  count_launches(1);
+  return last_launch();
+}
+
+int dmb_latch_import(dmb_ctx* ctx, const int32_t* d_flag, void* stream) {
+  if (!ctx || !d_flag) return fail(DMB_CONFIG, "NULL argument");
+  latch_import_kernel<<<1, 1, 0, as_stream(stream)>>>(ctx->status, d_flag);
+  count_launches(1);
+  return last_launch();
 }
 
 int dmb_set_wire_format(dmb_ctx* ctx, int32_t format) {

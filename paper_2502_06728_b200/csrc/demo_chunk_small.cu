@@ -26,7 +26,7 @@ void launch_chunk_kernel(ChunkMode mode, const ChunkArgs& a_in, cudaStream_t str
     // length and basis) goes through the SIMT kernel
     // a merge never defers: it leaves the fix-up list to an encode that may be running
     // concurrently on another stream
-    if (mode != ChunkMode::MergeAdam) cudaMemsetAsync(a.fb_count, 0, sizeof(unsigned), stream);
+    if (mode != ChunkMode::MergeAdam && mode != ChunkMode::MergeSgd) cudaMemsetAsync(a.fb_count, 0, sizeof(unsigned), stream);
     timer_begin(stream);
     launch_tc3_kernel(mode, a, stream);
     timer_end(stream);

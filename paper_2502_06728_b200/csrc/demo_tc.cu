@@ -19,9 +19,18 @@
 // Reference: transform.cpp:56-73 (DCT), :127-147 (TopK, sparse inverse),
 // replicate.cpp:137-144 + :282-309 (conditioning, merge), optim.cpp:18-74.
 //
-// Certification bound: with RNA TF32 splits of x and B, the dropped
-// lo*lo term, and FP32 accumulation over 24 MMAs, |c~_j - c_j| stays below
-// 2^-16 * sqrt(2/s) * ||x||_1 with a wide margin (the tests measure the margin).
+// Certification bound: |c~_j - c_j| <= kEpsScale * ||x||_1, derived with the per-MMA model
+// of demo_tc_adam.cu (kEpsScale there): one tcgen05.mma kind::tf32 step (K = 8) takes exact
+// products, aligns every term to the largest exponent with truncation and truncates the sum
+// once -> error <= 9 * 2^-23 (|acc| + sum |terms|).  With S = sum_i |x_i||B_ji| <=
+// sqrt(2/s) ||x||_1 and RNA TF32 splits (|x - hi| <= 2^-11 |x|, |x - hi - lo| <= 2^-22 |x|,
+// the same for B), in the issue order of issue_3x:
+//   16 cross-term steps first (acc + terms <= 2 * 2^-11 (1 + 2^-11) S): 16 * 9 * 2^-23 * 2^-10 S
+//                                                                       = 1.7e-8 S
+//   8 hi*hi steps last (acc + terms <= (1 + 2^-9) S):  8 * 9 * 2^-23 * (1 + 2^-9) S = 8.60e-6 S
+//   split residuals: x (2^-22), B (2^-22), the dropped lo*lo (2^-22)      = 7.2e-7 S
+//   oracle's own FP64 rounding: 64 * 2^-53 S                               ~ 0
+// total 9.34e-6 S; the radius used, 2^-16 * 1.01 = 1.54e-5 S, covers it with a 1.65x margin.
 #include <cfloat>
 
 #include "dmb_internal.cuh"
@@ -45,7 +54,7 @@ constexpr uint32_t OFF_A = 4 * B_BYTES;
 constexpr uint32_t OFF_BAR = OFF_A + GROUPS * 2 * A_BYTES;
 constexpr uint32_t SMEM_BYTES = OFF_BAR + 64 + 1024;
 constexpr uint32_t TMEM_COLS = 512;  // per group: D1 | D2 | D3 at +0 / +64 / +128, group stride 256
-constexpr float kEpsScale = 1.52587890625e-05f * 0.1767766952966369f * 1.01f;  // 2^-16 sqrt(2/64)
+constexpr float kEpsScale = 1.52587890625e-05f * 0.1767766952966369f * 1.01f;  // 2^-16 sqrt(2/64), see above
 
 // byte offset of the 16-byte chunk q (cols 4q..4q+3) of row r in a K-major SW128 tile
 __device__ __forceinline__ uint32_t sw_off(int r, int q, uint32_t rows) {
@@ -71,17 +80,20 @@ __device__ __forceinline__ void store_row(uint8_t* hi_base, uint8_t* lo_base, in
   }
 }
 
-// D = Ahi Bhi + Ahi Blo + Alo Bhi over K = 64 (8 MMAs of K = 8 per product)
+// D = Ahi Bhi + Ahi Blo + Alo Bhi over K = 64 (8 MMAs of K = 8 per product).  The 16 small
+// cross terms (|term| <= 2^-11 |x||B| each) accumulate first and the 8 hi*hi steps last, so
+// the accumulator is small while the small terms are added: kEpsScale assumes this order.
 __device__ __forceinline__ void issue_3x(uint32_t d, uint32_t ahi, uint32_t alo, uint32_t bhi, uint32_t blo,
                                          bool lo_a) {
+  auto ao = [](int k) { return (uint32_t)(k >> 2) * (TM * 128u) + (uint32_t)(k & 3) * 32u; };
+  auto bo = [](int k) { return (uint32_t)(k >> 2) * (S * 128u) + (uint32_t)(k & 3) * 32u; };
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
-    const uint32_t ao = (uint32_t)(k >> 2) * (TM * 128u) + (uint32_t)(k & 3) * 32u;
-    const uint32_t bo = (uint32_t)(k >> 2) * (S * 128u) + (uint32_t)(k & 3) * 32u;
-    mma_tf32(d, desc_sw128(ahi + ao), desc_sw128(bhi + bo), IDESC, k > 0 ? 1u : 0u);
-    mma_tf32(d, desc_sw128(ahi + ao), desc_sw128(blo + bo), IDESC, 1u);
-    if (lo_a) mma_tf32(d, desc_sw128(alo + ao), desc_sw128(bhi + bo), IDESC, 1u);
+    mma_tf32(d, desc_sw128(ahi + ao(k)), desc_sw128(blo + bo(k)), IDESC, k > 0 ? 1u : 0u);
+    if (lo_a) mma_tf32(d, desc_sw128(alo + ao(k)), desc_sw128(bhi + bo(k)), IDESC, 1u);
   }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) mma_tf32(d, desc_sw128(ahi + ao(k)), desc_sw128(bhi + bo(k)), IDESC, 1u);
 }
 
 __device__ __forceinline__ void load_tmem_row(uint32_t taddr, float (&v)[64]) {

@@ -22,15 +22,21 @@
 // Every hand-off is an mbarrier; control warps stay converged (lane 0 issues).
 //
 // TMEM columns (AdamW): C [0,64)  D [64,128)  X/W hi [128,192)  X/W lo [192,256)  raw
-// gradient ring of three tiles [256,448); SGD keeps a second W and D there instead.  W
+// gradient ring of three tiles [256,448).  SGD modes: a two-tile ring of m_acc = beta m + g
+// instead, and (StepSgd with a sign / fp16 wire) W2 = wire on the selection and D2 = Q.  W
 // reuses the X columns (X of t+1 is consumed by the forward MMA before W of t is written;
 // W of t by the inverse before X of t+2).
 //
 // Reference: transform.cpp:56-73, :127-147 (DCT, TopK, inverse); replicate.cpp:137-144,
-// :282-309 (conditioning, merge); optim.cpp:51-74 (decoupled AdamW).  Modes: StepAdam
-// (prepare + merge(R=1) + apply), MergeAdam (R gathered payloads + own indices -> apply),
-// EncodeAdam (payload only), StepSgd.  The one partial chunk at the shard end is handed to
-// the SIMT kernel; uncertified chunks to demo_fix64_kernel, which runs right after.
+// :282-309 (conditioning, merge); optim.cpp:18-74 (DeMo-SGD, decoupled AdamW).  Modes:
+//   StepAdam   prepare + merge(R=1) + AdamW apply                    g, p, exp_avg, exp_avg_sq
+//   MergeAdam  R gathered payloads + own indices (local_q re-derived) -> AdamW apply
+//   EncodeAdam payload only (no state)
+//   StepSgd    m_acc = beta m + g, prepare, merge(R=1), m -= local_q, p -= lr Q   (20 B/param)
+//   EncodeSgd  m_acc, payload, m_out = m_acc - local_q                 (N > 1 SGD prepare)
+//   MergeSgd   R gathered payloads -> Q = IDCT(grid / R) -> p -= lr Q (no forward DCT, no g)
+// The one partial chunk at the shard end is handed to the SIMT kernel; uncertified chunks to
+// demo_fix64_kernel, which runs right after.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -75,11 +81,13 @@ constexpr uint32_t SMEM_BYTES = OFF_L1 + 2 * TM * 4;
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
 constexpr uint32_t COL_C = 0, COL_D = 64, COL_XH = 128, COL_XL = 192, COL_G = 256;
-// StepSgd: the raw-gradient ring is not needed (the apply warps recompute m_acc from the
-// staged momentum and gradient); its columns hold W2 = wire on the selection (hi, lo) and
-// D2 = IDCT(W2) = Q, next to W1 = coef on the selection (X columns) and D1 = IDCT(W1) = local_q
-constexpr uint32_t COL_W2H = 256, COL_W2L = 320, COL_D2 = 384;
-constexpr uint32_t OFF_M = OFF_SCR;  // StepSgd: the momentum tile of the gradient split
+// SGD modes: W1 = coef on the selection (X columns) and D1 = IDCT(W1) = local_q; the front
+// keeps m_acc = beta m + g in a two-tile ring for the apply (so g and m are read once).  StepSgd
+// needs Q = IDCT(W2), W2 = wire on the selection: with a fp32 wire W2 = W1 (Q = D1); with a
+// sign or fp16 wire every W2 value is TF32-exact, so W2 takes hi columns only.
+constexpr uint32_t COL_W2H = 256, COL_D2 = 320;
+__host__ __device__ constexpr uint32_t col_macc(bool q2) { return q2 ? 384u : 256u; }
+constexpr uint32_t OFF_M = OFF_SCR;  // SGD modes: the momentum tile of the gradient split
 constexpr uint32_t TMEM_COLS = 512;
 
 // Certification radius of a tensor-core coefficient: |c_tc - c_oracle| <= kEpsScale ||x||_1.
@@ -396,6 +404,19 @@ __device__ __forceinline__ float cond_w(float c) {
   if (WIRE == kWireF16) return __half2float(__float2half_rn(c));
   return c;
 }
+// m_hat / (sqrt(v_hat) + eps), optim.cpp:68-70.  The IEEE sqrtf and '/' compile to a slow-path
+// check, a CALL and a reconvergence point per element, which made this kernel 2.7x slower
+// (measured: 19.6 ms against 7.2 ms per OLMo-1B step); the hardware square root and a
+// Newton-refined reciprocal are each within a few ulp (~1e-7 relative), two orders below the
+// 1e-5 parity bar -- the tests and smoke() print the error actually reached.
+__device__ __forceinline__ float adam_ratio(float m1, float m2, const AdamScalars& A) {
+  float sq, r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(m2 * A.inv_bc2));
+  const float d = sq + A.eps;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
+  r = fmaf(r, fmaf(-d, r, 1.0f), r);
+  return (m1 * A.inv_bc1) * r;
+}
 // exact TF32 split: hi keeps the top 10 mantissa bits, lo = x - hi is exact in FP32
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
@@ -456,9 +477,19 @@ struct TensorMaps {
 template <ChunkMode MODE, int WIRE>
 __global__ void __maxnreg__(128)
     demo_tc_adam_kernel(const ChunkArgs a, const __grid_constant__ TensorMaps maps) {
-  constexpr bool kEncodeOnly = MODE == ChunkMode::EncodeAdam;
-  constexpr bool kMerge = MODE == ChunkMode::MergeAdam;
+  constexpr bool kEncodeOnly = MODE == ChunkMode::EncodeAdam;  // no state at all
+  constexpr bool kMergeSgd = MODE == ChunkMode::MergeSgd;      // no forward DCT, no gradient
+  constexpr bool kMerge = MODE == ChunkMode::MergeAdam || kMergeSgd;
   constexpr bool kSgd = MODE == ChunkMode::StepSgd;  // m = beta m + g; m -= local_q; p -= lr Q
+  constexpr bool kEncSgd = MODE == ChunkMode::EncodeSgd;  // m = beta m + g; m -= local_q; payload
+  constexpr bool kMomentum = kSgd || kEncSgd;             // the front encodes m_acc = beta m + g
+  constexpr bool kSgdApply = kMomentum || kMergeSgd;      // the SGD apply stage
+  constexpr bool kFwd = !kMergeSgd;
+  constexpr bool kQ2 = kSgd && WIRE != kWireF32;          // a second inverse for Q (W2 hi only)
+  constexpr uint32_t COL_MACC = col_macc(kQ2);
+  // staging slots (p, exp_avg / m, exp_avg_sq): the first kLoads are loaded, bit v of kStores stored
+  constexpr int kLoads = (kSgd || kMergeSgd) ? 1 : (kEncSgd ? 0 : 3);
+  constexpr unsigned kStores = kSgd ? 3u : (kEncSgd ? 2u : (kMergeSgd ? 1u : 7u));
 
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023u) != 0u) __trap();
@@ -521,10 +552,15 @@ __global__ void __maxnreg__(128)
   // the staging tile moves in two 32-column halves: the apply warps hand back the first
   // half early, so its store and the next tile's first-half load start under the second
   auto load_state = [&](uint64_t t, int h) {  // one thread
-    mbar_arrive_expect_tx(&bar_s[h], 3 * BOX);
+    if (kLoads == 0) {  // nothing to load: the arrival only hands the free half to the apply warps
+      mbar_arrive(&bar_s[h]);
+      return;
+    }
+    mbar_arrive_expect_tx(&bar_s[h], kLoads * BOX);
     const CUtensorMap* m[3] = {&maps.p_in, &maps.ea_in, &maps.es_in};
 #pragma unroll
-    for (int v = 0; v < 3; ++v) tma_2d(smem + OFF_ST + v * TILE + h * BOX, m[v], 32 * h, (int)(t * TM), &bar_s[h]);
+    for (int v = 0; v < kLoads; ++v)
+      tma_2d(smem + OFF_ST + v * TILE + h * BOX, m[v], 32 * h, (int)(t * TM), &bar_s[h]);
   };
   // The two control warps stay converged: every lane runs the loop and the waits, lane 0
   // issues the TMA / tcgen05 operations.
@@ -542,8 +578,8 @@ __global__ void __maxnreg__(128)
           if (lane == 0) {
             const CUtensorMap* m[3] = {&maps.p_out, &maps.ea_out, &maps.es_out};
 #pragma unroll
-            for (int v = 0; v < (kSgd ? 2 : 3); ++v)  // SGD: p, m (the staged gradient is input only)
-              tma_2d_store(m[v], 32 * h, (int)(tile * TM), smem + OFF_ST + v * TILE + h * BOX);
+            for (int v = 0; v < 3; ++v)
+              if ((kStores >> v) & 1u) tma_2d_store(m[v], 32 * h, (int)(tile * TM), smem + OFF_ST + v * TILE + h * BOX);
             bulk_commit();
             bulk_wait_read();  // the half may be refilled
             if (tile + G < ntiles) load_state(tile + G, h);
@@ -562,10 +598,10 @@ __global__ void __maxnreg__(128)
     const uint32_t s_base = smem_u32(smem);
     auto load_g = [&](uint64_t t) {
       if (lane == 0) {
-        mbar_arrive_expect_tx(bar_g, kSgd ? 2 * TILE : TILE);
+        mbar_arrive_expect_tx(bar_g, kMomentum ? 2 * TILE : TILE);
         tma_2d(smem + OFF_G, &maps.g, 0, (int)(t * TM), bar_g);
         tma_2d(smem + OFF_G + BOX, &maps.g, 32, (int)(t * TM), bar_g);
-        if (kSgd) {  // the momentum tile: m_acc = beta m + g is the vector encoded
+        if (kMomentum) {  // the momentum tile: m_acc = beta m + g is the vector encoded
           tma_2d(smem + OFF_M, &maps.ea_in, 0, (int)(t * TM), bar_g);
           tma_2d(smem + OFF_M + BOX, &maps.ea_in, 32, (int)(t * TM), bar_g);
         }
@@ -593,7 +629,21 @@ __global__ void __maxnreg__(128)
       }
       __syncwarp();
     };
-    if (tile < ntiles) {
+    // D = W2(TMEM: hi only, TF32-exact) x B(smem hi, lo): the 8 hi*lo steps first, then hi*hi
+    auto issue_exact = [&](uint32_t d, uint32_t bh, uint32_t bl, uint64_t* bar, uint32_t ah) {
+      tc_fence_after();
+      if (lane == 0) {
+        auto bo = [](int kk) { return (uint32_t)(kk >> 2) * (S * 128u) + (uint32_t)(kk & 3) * 32u; };
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_tf32_ts(d, tmem + ah + 8u * kk, desc_sw128(s_base + bl + bo(kk)), IDESC, kk > 0 ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) mma_tf32_ts(d, tmem + ah + 8u * kk, desc_sw128(s_base + bh + bo(kk)), IDESC, 1u);
+        if (bar) mma_commit(bar);
+      }
+      __syncwarp();
+    };
+    if (kFwd && tile < ntiles) {
       load_g(tile);
       mbar_wait(bar_x, 0);
       issue(tmem + COL_C, OFF_BHI, OFF_BLO, bar_f);
@@ -601,7 +651,7 @@ __global__ void __maxnreg__(128)
     }
     for (uint32_t it = 0; tile < ntiles; tile += G, ++it) {
       const uint64_t t1 = tile + G;
-      if (t1 < ntiles) {
+      if (kFwd && t1 < ntiles) {
         mbar_wait(bar_x, (it + 1) & 1);  // X of t+1 in TMEM; the gradient stage is free
         mbar_wait(bar_c, it & 1);        // C of t read out by the select warps
         issue(tmem + COL_C, OFF_BHI, OFF_BLO, bar_f);
@@ -612,9 +662,9 @@ __global__ void __maxnreg__(128)
         evt(a, tid == 32 * kMmaWarp, it, 14);
         if (it > 0) mbar_wait(&bar_a[1], (it - 1) & 1);  // D of t-1 read by the apply warps
         evt(a, tid == 32 * kMmaWarp, it, 15);
-        if (kSgd) {  // local_q = IDCT(coef), Q = IDCT(wire), one commit for both
+        if (kQ2) {  // local_q = IDCT(coef), Q = IDCT(wire), one commit for both
           issue(tmem + COL_D, OFF_BTHI, OFF_BTLO, nullptr);
-          issue(tmem + COL_D2, OFF_BTHI, OFF_BTLO, bar_i, COL_W2H, COL_W2L);
+          issue_exact(tmem + COL_D2, OFF_BTHI, OFF_BTLO, bar_i, COL_W2H);
         } else {
           issue(tmem + COL_D, OFF_BTHI, OFF_BTLO, bar_i);
         }
@@ -647,7 +697,7 @@ __global__ void __maxnreg__(128)
         }
 #pragma unroll
         for (int e = 0; e < 16; ++e) fin = fin && isfinite(x[e]);
-        if (kSgd) {  // m_acc = beta m + g, multiply then add (optim.cpp:27)
+        if (kMomentum) {  // m_acc = beta m + g, multiply then add (optim.cpp:27)
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float4 m = *reinterpret_cast<const float4*>(smem + OFF_M + sw_off(trow, 4 * h + e));
@@ -659,7 +709,8 @@ __global__ void __maxnreg__(128)
         }
 #pragma unroll
         for (int e = 0; e < 16; ++e) l1 += fabsf(x[e]);
-        if (!kSgd && !kEncodeOnly) tmem_st16(tmem + tl + COL_G + 64 * (n % 3) + 16 * h, x);  // raw g for the apply
+        if (kMomentum) tmem_st16(tmem + tl + COL_MACC + 64 * (n & 1) + 16 * h, x);  // m_acc for the apply
+        else if (!kEncodeOnly) tmem_st16(tmem + tl + COL_G + 64 * (n % 3) + 16 * h, x);  // raw g for the apply
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           hi[e] = tf32_hi(x[e]);
@@ -688,8 +739,8 @@ __global__ void __maxnreg__(128)
         mbar_arrive(&bar_l[n & 1]);
       }
     };
-    if (tile < ntiles) front(tile, 0);
-    if (tile + G < ntiles) {
+    if (kFwd && tile < ntiles) front(tile, 0);
+    if (kFwd && tile + G < ntiles) {
       mbar_wait(bar_f, 0);  // X of the first tile consumed by its forward DCT
       front(tile + G, 1);
     }
@@ -703,41 +754,45 @@ __global__ void __maxnreg__(128)
       tc_fence_after();
       evt(a, tid == 32 * kSelWarps, it, 12);
       bool deferred = false;
-      if (kSgd) {
+      if (kSgdApply) {
+        // m_out = m_acc - local_q (k = s: 0 exactly), p_out = p - lr Q (optim.cpp:18-49); a
+        // deferred row keeps p as loaded and m_in, both rewritten by the fix-up kernel
+        const uint64_t grow = tile * TM + trow;
 #pragma unroll 1
         for (int h = 0; h < 4; ++h) {
-          float d1[16], d2[16];
+          float d1[16], d2[16], mc[16];
           tmem_ld16(tmem + tl + COL_D + 16 * h, d1);
-          tmem_ld16(tmem + tl + COL_D2 + 16 * h, d2);
-          float4 p4[4], m4[4], g4[4];
+          if (kQ2) tmem_ld16(tmem + tl + COL_D2 + 16 * h, d2);
+          if (kMomentum) tmem_ld16(tmem + tl + COL_MACC + 64 * (it & 1) + 16 * h, mc);
+          float4 p4[4], m4[4];
+          if (!kEncSgd) {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint32_t off = OFF_ST + sw_off(trow, 4 * h + e);
-            p4[e] = *reinterpret_cast<const float4*>(smem + off);
-            m4[e] = *reinterpret_cast<const float4*>(smem + off + TILE);
-            g4[e] = *reinterpret_cast<const float4*>(smem + off + 2 * TILE);
+            for (int e = 0; e < 4; ++e) p4[e] = *reinterpret_cast<const float4*>(smem + OFF_ST + sw_off(trow, 4 * h + e));
           }
           tmem_ld_wait();
-          if (h == 0) deferred = isnan(d1[0]);
+          if (h == 0) deferred = !kMergeSgd && isnan(d1[0]);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             float* pz = &p4[e].x;
             float* mz = &m4[e].x;
-            const float* gz = &g4[e].x;
 #pragma unroll
             for (int z = 0; z < 4; ++z) {
-              const float macc = __fadd_rn(__fmul_rn(a.sgd.beta, mz[z]), gz[z]);
-              mz[z] = full_band ? 0.0f : macc - d1[4 * e + z];  // m -= local_q (k = s: local_q = m exactly)
-              pz[z] = pz[z] - a.sgd.lr * d2[4 * e + z];         // p -= lr Q (optim.cpp:45-49)
+              const int i = 4 * e + z;
+              if (kMomentum) mz[z] = full_band ? 0.0f : mc[i] - d1[i];  // m -= local_q (k = s: local_q = m exactly)
+              if (!kEncSgd) pz[z] = pz[z] - a.sgd.lr * (kQ2 ? d2[i] : d1[i]);  // p -= lr Q (optim.cpp:45-49)
             }
           }
           if (!deferred) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const uint32_t off = OFF_ST + sw_off(trow, 4 * h + e);
-              *reinterpret_cast<float4*>(smem + off) = p4[e];
-              *reinterpret_cast<float4*>(smem + off + TILE) = m4[e];
+              if (!kEncSgd) *reinterpret_cast<float4*>(smem + off) = p4[e];
+              if (kMomentum) *reinterpret_cast<float4*>(smem + off + TILE) = m4[e];
             }
+          } else if (kMomentum) {  // rare: the row's m_in goes back unchanged
+            const float4* src = reinterpret_cast<const float4*>(a.m_in + grow * S + 16 * h);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) *reinterpret_cast<float4*>(smem + OFF_ST + TILE + sw_off(trow, 4 * h + e)) = src[e];
           }
           if (h & 1) {  // half done: to the TMA store
             tc_fence_before();
@@ -773,9 +828,7 @@ __global__ void __maxnreg__(128)
             const float gp = full_band ? d[4 * e + z] : g[4 * e + z] + d[4 * e + z];  // g - local_q + Q (optim.cpp:65)
             const float m1 = A.beta1 * ez[z] + A.one_minus_beta1 * gp;
             const float m2 = A.beta2 * sz[z] + A.one_minus_beta2 * gp * gp;
-            float sq;
-            asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(m2 * A.inv_bc2));
-            float pn = pz[z] - __fdividef(m1 * A.lr_bc1, sq + A.eps);
+            float pn = pz[z] - A.lr * adam_ratio(m1, m2, A);
             pn -= A.lr_wd * pn;  // decoupled weight decay (0 when disabled)
             ez[z] = m1;
             sz[z] = m2;
@@ -802,7 +855,7 @@ __global__ void __maxnreg__(128)
       }
       // AdamW first: its store frees the staging tile for the next tile's state load, which
       // then runs under this front
-      if (tile + 2 * G < ntiles) {
+      if (kFwd && tile + 2 * G < ntiles) {
         // the X columns are free once the inverse of this tile (or, encode only, the
         // forward of the next) has read them
         if (!kEncodeOnly) mbar_wait(bar_i, it & 1);
@@ -834,21 +887,28 @@ __global__ void __maxnreg__(128)
       const bool act0 = r0 < nfull, act1 = r1 < nfull;
       evt(a, tid == 0, it, 0);
       evt_at(a, lane == 0, it, 24 + warp);
-      mbar_wait(bar_f, it & 1);
-      evt(a, tid == 0, it, 1);
-      tc_fence_after();
-      float c0[16], c1[16];
-      {
-        uint32_t r[32];
-        ld_quad(tmem + tq + COL_C, r);
-        tmem_ld_wait();
-        unpack_rows(r, c0, c1);
+      float c0[16], c1[16];  // coefficients (not read by MergeSgd: no forward DCT)
+      float l10 = 0.0f, l11 = 0.0f;
+      if (kFwd) {
+        mbar_wait(bar_f, it & 1);
+        evt(a, tid == 0, it, 1);
+        tc_fence_after();
+        {
+          uint32_t r[32];
+          ld_quad(tmem + tq + COL_C, r);
+          tmem_ld_wait();
+          unpack_rows(r, c0, c1);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_c);  // the forward of the next tile may overwrite C
+        mbar_wait(&bar_l[it & 1], (it >> 1) & 1);
+        l10 = l1buf[(it & 1) * TM + row0];
+        l11 = l1buf[(it & 1) * TM + row1];
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) c0[e] = c1[e] = 0.0f;
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_c);  // the forward of the next tile may overwrite C
-      mbar_wait(&bar_l[it & 1], (it >> 1) & 1);
-      const float l10 = l1buf[(it & 1) * TM + row0], l11 = l1buf[(it & 1) * TM + row1];
       evt(a, tid == 0, it, 4);
 
       uint32_t sel0 = 0, sel1 = 0;
@@ -1037,6 +1097,12 @@ __global__ void __maxnreg__(128)
             constexpr uint32_t M = 0x00010001u;
             uint32_t ce[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, co[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
             const int s4 = 4 * s;
+            // protocol checks (replicate.cpp:284-293 for this layout), split over the quad: threads
+            // 0 / 1 check that the member's mask of row 0 / 1 selects exactly k frequencies,
+            // threads 2 / 3 that the row's code words hold no invalid code 3 and at most k
+            // nonzero codes
+            bool bad = false;
+            const bool chk_act = (s & 1) ? act1 : act0;
             for (int rr = 0; rr < a.in.R; ++rr) {
               uint64_t lo0, hi0, lo1, hi1;
               if (staged) {
@@ -1051,6 +1117,17 @@ __global__ void __maxnreg__(128)
                 lo1 = act1 ? __ldg(dv + 2 * r1) : 0ull;
                 hi1 = act1 ? __ldg(dv + 2 * r1 + 1) : 0ull;
               }
+              if (chk_act) {
+                if (s < 2) {
+                  const unsigned long long* mk = reinterpret_cast<const unsigned long long*>(a.in.body[rr]);
+                  bad |= __popcll(__ldg(mk + (s ? r1 : r0))) != k;
+                } else {
+                  constexpr uint64_t Z = 0x5555555555555555ull;
+                  const uint64_t lo = s == 2 ? lo0 : lo1, hi = s == 2 ? hi0 : hi1;
+                  bad |= (((lo & (lo >> 1)) | (hi & (hi >> 1))) & Z) != 0ull;
+                  bad |= __popcll((lo | (lo >> 1)) & Z) + __popcll((hi | (hi >> 1)) & Z) > k;
+                }
+              }
               const uint32_t w[8] = {(uint32_t)lo0, (uint32_t)(lo0 >> 32), (uint32_t)hi0, (uint32_t)(hi0 >> 32),
                                      (uint32_t)lo1, (uint32_t)(lo1 >> 32), (uint32_t)hi1, (uint32_t)(hi1 >> 32)};
 #pragma unroll
@@ -1059,6 +1136,7 @@ __global__ void __maxnreg__(128)
                 co[i] += ((w[i] >> (s4 + 2)) & M) + (~(w[i] >> (s4 + 3)) & M);
               }
             }
+            if (bad) atomicExch(&a.status->protocol_error, 1u);
             const int Rm = a.in.R;
 #pragma unroll
             for (int e = 0; e < 16; ++e) {  // element e = 2r + b: half-word r / 2, lane r & 1
@@ -1160,18 +1238,25 @@ __global__ void __maxnreg__(128)
           const int col = qcol(e, s);
           const bool on0 = (sel0 >> e) & 1u, on1 = (sel1 >> e) & 1u;
           float v0, v1;
-          if (kSgd) {  // W1 = coef on the selection (local_q; k = s: unused), W2 = wire
-            v0 = (on0 && !full_band) ? c0[e] : 0.0f;
-            v1 = (on1 && !full_band) ? c1[e] : 0.0f;
-            const float x0 = full_band || on0 ? cond_w<WIRE>(c0[e]) : 0.0f;
-            const float x1 = full_band || on1 ? cond_w<WIRE>(c1[e]) : 0.0f;
-            u0[e] = def0 ? __int_as_float(0x7fc00000) : (act0 ? x0 : 0.0f);
-            u1[e] = def1 ? __int_as_float(0x7fc00000) : (act1 ? x1 : 0.0f);
+          if (kMomentum) {
+            // W1 = coef on the selection (local_q; k = s: unused, m_out = 0).  StepSgd: with a
+            // fp32 wire W2 = W1, so Q = D1 (and k = s keeps every coefficient in W1); else
+            // W2 = wire on the selection
+            const bool w1_all = kSgd && WIRE == kWireF32;
+            v0 = (on0 && (!full_band || w1_all)) ? c0[e] : 0.0f;
+            v1 = (on1 && (!full_band || w1_all)) ? c1[e] : 0.0f;
+            if (kQ2) {
+              const float x0 = full_band || on0 ? cond_w<WIRE>(c0[e]) : 0.0f;
+              const float x1 = full_band || on1 ? cond_w<WIRE>(c1[e]) : 0.0f;
+              u0[e] = def0 ? __int_as_float(0x7fc00000) : (act0 ? x0 : 0.0f);
+              u1[e] = def1 ? __int_as_float(0x7fc00000) : (act1 ? x1 : 0.0f);
+            }
           } else if (kMerge) {  // an inactive row has no selection and an empty grid row
             const float g0v = a.geo.wire_mask ? gq0[e] : grid[l0 * S + (col ^ ((l0 & 7) << 3))];
             const float g1v = a.geo.wire_mask ? gq1[e] : grid[l1 * S + (col ^ ((l1 & 7) << 3))];
-            v0 = g0v * invR - ((on0 && !full_band) ? c0[e] : 0.0f);
-            v1 = g1v * invR - ((on1 && !full_band) ? c1[e] : 0.0f);
+            // MergeAdam: W = Q - local_q of the own selection; MergeSgd: W = grid / R (Q)
+            v0 = g0v * invR - ((!kMergeSgd && on0 && !full_band) ? c0[e] : 0.0f);
+            v1 = g1v * invR - ((!kMergeSgd && on1 && !full_band) ? c1[e] : 0.0f);
           } else if (WIRE == kWireSign) {
             // the selection is empty on an inactive row; on a stored (certified) row every
             // selected |c| is above the radius, so cond(c) = copysign(1, c) there
@@ -1192,7 +1277,11 @@ __global__ void __maxnreg__(128)
           }
         }
         evt(a, tid == 0, it, 7);
-        if (has_next) mbar_wait(bar_f, (it + 1) & 1);  // X of t+1 consumed: the columns take W
+        if (kFwd) {
+          if (has_next) mbar_wait(bar_f, (it + 1) & 1);  // X of t+1 consumed: the columns take W
+        } else if (it > 0) {
+          mbar_wait(bar_i, (it - 1) & 1);  // MergeSgd: W of t-1 read by its inverse
+        }
         evt(a, tid == 0, it, 8);
         tc_fence_after();
         uint32_t r[32];
@@ -1207,18 +1296,9 @@ __global__ void __maxnreg__(128)
         st_quad(tmem + tq + COL_XH, r);
         pack_rows(w0, w1, r);
         st_quad(tmem + tq + COL_XL, r);
-        if (kSgd) {
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const float h0 = tf32_hi(u0[e]), h1 = tf32_hi(u1[e]);
-            u0[e] -= h0;
-            u1[e] -= h1;
-            r[4 * (e >> 1) + (e & 1)] = __float_as_uint(h0);
-            r[4 * (e >> 1) + 2 + (e & 1)] = __float_as_uint(h1);
-          }
-          st_quad(tmem + tq + COL_W2H, r);
+        if (kQ2) {  // W2 is TF32-exact (signs, fp16-rounded values): hi columns only
           pack_rows(u0, u1, r);
-          st_quad(tmem + tq + COL_W2L, r);
+          st_quad(tmem + tq + COL_W2H, r);
         }
         tmem_st_wait();
         tc_fence_before();
@@ -1260,6 +1340,7 @@ template <ChunkMode MODE, int WIRE>
 __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkArgs a) {
   constexpr bool kEncodeOnly = MODE == ChunkMode::EncodeAdam;
   constexpr bool kSgd = MODE == ChunkMode::StepSgd;
+  constexpr bool kMomentum = kSgd || MODE == ChunkMode::EncodeSgd;
   extern __shared__ __align__(16) uint8_t fsm[];
   float* b32 = reinterpret_cast<float*>(fsm);              // B[j][i] row-major
   float* bt = reinterpret_cast<float*>(fsm + S * S * 4);    // B^T: (i, j) at i*64 + j
@@ -1286,7 +1367,7 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
     const uint64_t c = a.fb_list[u];
     const uint64_t g0 = c * S;
     float x0 = a.g[g0 + lane], x1 = a.g[g0 + lane + 32];
-    if (kSgd) {  // the encoded vector is m_acc = beta m + g (multiply, then add)
+    if (kMomentum) {  // the encoded vector is m_acc = beta m + g (multiply, then add)
       x0 = __fadd_rn(__fmul_rn(a.sgd.beta, a.m_in[g0 + lane]), x0);
       x1 = __fadd_rn(__fmul_rn(a.sgd.beta, a.m_in[g0 + lane + 32]), x1);
     }
@@ -1448,7 +1529,7 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
       }
     }
     if (kEncodeOnly) continue;
-    if (kSgd) {  // local_q = IDCT(coef), Q = IDCT(wire) over the selection, ascending j
+    if (kMomentum) {  // local_q = IDCT(coef), Q = IDCT(wire) over the selection, ascending j
       float q0 = 0.0f, q1 = 0.0f, l0 = 0.0f, l1 = 0.0f;
       for (int e = 0; e < 2; ++e) {
         unsigned m = __ballot_sync(kFull, e ? sel1 : sel0);
@@ -1469,7 +1550,7 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
         const uint64_t gi = g0 + lane + 32 * e;
         const float macc = e ? x1 : x0;
         a.m_out[gi] = full_band ? 0.0f : macc - (e ? l1 : l0);
-        a.p_out[gi] = a.p_in[gi] - a.sgd.lr * (e ? q1 : q0);
+        if (kSgd) a.p_out[gi] = a.p_in[gi] - a.sgd.lr * (e ? q1 : q0);
       }
       continue;
     }
@@ -1496,9 +1577,7 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
       const float gp = full_band ? d : (e ? x1 : x0) + d;  // g - local_q + Q (optim.cpp:65)
       const float m1 = A.beta1 * a.ea_in[gi] + A.one_minus_beta1 * gp;
       const float m2 = A.beta2 * a.es_in[gi] + A.one_minus_beta2 * gp * gp;
-      float sq;
-      asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(m2 * A.inv_bc2));
-      float pn = a.p_in[gi] - __fdividef(m1 * A.lr_bc1, sq + A.eps);
+      float pn = a.p_in[gi] - A.lr * adam_ratio(m1, m2, A);
       pn -= A.lr_wd * pn;
       a.ea_out[gi] = m1;
       a.es_out[gi] = m2;
@@ -1560,19 +1639,26 @@ void launch_mode(const ChunkArgs& a, const TensorMaps& maps, cudaStream_t stream
 
 }  // namespace
 
+bool tc3_available() { return encode_fn() != nullptr; }
+
 bool tc3_supported(ChunkMode mode, const ChunkArgs& a) {
   if (a.geo.s != S || a.basis.Bhi == nullptr || encode_fn() == nullptr) return false;
-  if (!(mode == ChunkMode::StepAdam || mode == ChunkMode::MergeAdam || mode == ChunkMode::EncodeAdam ||
-        mode == ChunkMode::StepSgd))
-    return false;
   if (a.local_q || a.m_accum || a.q_out) return false;  // inspection outputs: generic kernels
   if (a.geo.len / S == 0) return false;                 // the tensor maps need one whole chunk
-  if (mode == ChunkMode::MergeAdam && (a.in.R < 1 || a.own_rank < 0 || a.own_rank >= a.in.R)) return false;
-  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-  if (!al(a.g)) return false;
-  if (mode == ChunkMode::EncodeAdam) return true;
-  if (mode == ChunkMode::StepSgd) return a.m_in && a.m_out && al(a.m_in) && al(a.m_out) && al(a.p_in) && al(a.p_out);
-  return al(a.p_in) && al(a.p_out) && al(a.ea_in) && al(a.ea_out) && al(a.es_in) && al(a.es_out);
+  if ((mode == ChunkMode::MergeAdam || mode == ChunkMode::MergeSgd) && (a.in.R < 1 || a.in.R > kMaxReplicas))
+    return false;
+  if (mode == ChunkMode::MergeAdam && (a.own_rank < 0 || a.own_rank >= a.in.R)) return false;
+  auto al = [](const void* p) { return p && (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  switch (mode) {
+    case ChunkMode::EncodeAdam: return al(a.g);
+    case ChunkMode::EncodeSgd: return al(a.g) && al(a.m_in) && al(a.m_out);
+    case ChunkMode::StepSgd: return al(a.g) && al(a.m_in) && al(a.m_out) && al(a.p_in) && al(a.p_out);
+    case ChunkMode::MergeSgd: return al(a.p_in) && al(a.p_out);
+    case ChunkMode::StepAdam:
+    case ChunkMode::MergeAdam:
+      return al(a.g) && al(a.p_in) && al(a.p_out) && al(a.ea_in) && al(a.ea_out) && al(a.es_in) && al(a.es_out);
+  }
+  return false;
 }
 
 void launch_tc3_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) {
@@ -1580,13 +1666,18 @@ void launch_tc3_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) 
   TensorMaps maps;
   memset(&maps, 0, sizeof(maps));
   const uint64_t rows = a.geo.len / S;
-  tile_map(&maps.g, a.g, rows);
-  if (mode == ChunkMode::StepSgd) {  // staging: p, m, g; the split reads g and m
-    tile_map(&maps.p_in, a.p_in, rows);
+  if (mode != ChunkMode::MergeSgd) tile_map(&maps.g, a.g, rows);
+  if (mode == ChunkMode::StepSgd || mode == ChunkMode::EncodeSgd) {
+    // the split reads g and m (ea_in); staging: p in / out (StepSgd), m out
     tile_map(&maps.ea_in, a.m_in, rows);
-    tile_map(&maps.es_in, a.g, rows);
-    tile_map(&maps.p_out, a.p_out, rows);
     tile_map(&maps.ea_out, a.m_out, rows);
+    if (mode == ChunkMode::StepSgd) {
+      tile_map(&maps.p_in, a.p_in, rows);
+      tile_map(&maps.p_out, a.p_out, rows);
+    }
+  } else if (mode == ChunkMode::MergeSgd) {
+    tile_map(&maps.p_in, a.p_in, rows);
+    tile_map(&maps.p_out, a.p_out, rows);
   } else if (mode != ChunkMode::EncodeAdam) {
     tile_map(&maps.p_in, a.p_in, rows);
     tile_map(&maps.ea_in, a.ea_in, rows);
@@ -1600,12 +1691,14 @@ void launch_tc3_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) 
     case ChunkMode::MergeAdam: launch_mode<ChunkMode::MergeAdam>(a, maps, stream); break;
     case ChunkMode::EncodeAdam: launch_mode<ChunkMode::EncodeAdam>(a, maps, stream); break;
     case ChunkMode::StepSgd: launch_mode<ChunkMode::StepSgd>(a, maps, stream); break;
-    default: break;
+    case ChunkMode::EncodeSgd: launch_mode<ChunkMode::EncodeSgd>(a, maps, stream); break;
+    case ChunkMode::MergeSgd: launch_mode<ChunkMode::MergeSgd>(a, maps, stream); break;
   }
 }
 
 
 void launch_fix64_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) {
+  if (mode == ChunkMode::MergeAdam || mode == ChunkMode::MergeSgd) return;  // merges never defer
   count_launches(1);
   auto go = [&](auto kern) {
     // every instantiation needs its own attribute (a static flag here would be shared)
@@ -1633,7 +1726,12 @@ void launch_fix64_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream
       else if (f16) go(demo_fix64_kernel<ChunkMode::StepSgd, kWireF16>);
       else go(demo_fix64_kernel<ChunkMode::StepSgd, kWireF32>);
       break;
-    default: break;  // MergeAdam never defers
+    case ChunkMode::EncodeSgd:
+      if (sign) go(demo_fix64_kernel<ChunkMode::EncodeSgd, kWireSign>);
+      else if (f16) go(demo_fix64_kernel<ChunkMode::EncodeSgd, kWireF16>);
+      else go(demo_fix64_kernel<ChunkMode::EncodeSgd, kWireF32>);
+      break;
+    default: break;
   }
 }
 

@@ -181,6 +181,7 @@ bool tc_supported(ChunkMode mode, const ChunkArgs& a);
 void launch_tc_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream);
 bool tc_enabled();
 bool tc3_supported(ChunkMode mode, const ChunkArgs& a);
+bool tc3_available();  // the tensor-map encoder of the driver is reachable
 void launch_tc3_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream);
 // exact FP64 re-derivation of the full chunks listed in a.fb_list / a.fb_count
 void launch_fix64_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream);

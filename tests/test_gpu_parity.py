@@ -10,10 +10,13 @@ Bars (stated here and in DESIGN.md):
   * fp16 wire values: within one binary16 ulp of the oracle's (the GPU rounds an FP32
     coefficient, the oracle an FP64 one).
 """
+import os
+
 import numpy as np
 import pytest
 import torch
 
+from tests._parity_log import record
 from oracle.oracle import DEMO, DILOCO, FP16, FP32, FULL, RANDOM, STRIDING, TERNARY, Rep
 
 pytestmark = pytest.mark.gpu
@@ -50,18 +53,38 @@ def chunk_close(got, want, s, tol=TOL, what=""):
     w = np.concatenate([want, np.zeros(pad)]).reshape(-1, s)
     scale = np.maximum(np.abs(w).max(axis=1), 1e-30)
     err = np.abs(g - w).max(axis=1) / scale
+    worst = float(err.max()) if len(err) else 0.0
+    record(os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], what or "value", worst, tol)
     bad = np.nonzero(err > tol)[0]
-    assert len(bad) == 0, f"{what}: {len(bad)} chunks over tol, worst {err.max():.3g} at chunk {bad[:5]}"
+    assert len(bad) == 0, f"{what}: {len(bad)} chunks over tol, worst {worst:.3g} at chunk {bad[:5]}"
+    return worst
 
 
-def update_close(p_got, p_want, p_before, lr, s, tol=1e-4, what="params"):
-    """AdamW parameters: the error of the applied update, relative to the chunk's largest
-    update.  g' = g - local_q + Q can cancel to ~0 inside a chunk whose scale is set by Q,
-    and Adam divides by sqrt(v_hat), so element-relative bars are meaningless there; the
-    update-relative bar is stated as 1e-4."""
-    u_want = (np.asarray(p_before, np.float64) - np.asarray(p_want, np.float64)) / lr
+UPDATE_TOL = 3e-5
+
+
+def update_close(p_got, p_want, p_before, lr, s, tol=TOL, what="params"):
+    """AdamW parameters.  The bar: p within 1e-5 of its chunk's L-inf (north_star's bar on
+    parameters).  A stricter diagnostic on top: the applied update u = (p_before - p) / lr
+    within 3e-5 of the chunk's largest |u|, beyond the FP32 rounding of the stored parameter
+    itself (the Adam step and the weight decay each round p to FP32: 2 x 2^-24 |p| / lr in
+    update units), which no FP32 parameter vector can resolve.  The ratio m_hat / sqrt(v_hat)
+    amplifies the ~1e-6 relative error of the FP32 Q = IDCT(merged grid) where v_hat is small,
+    so this bar sits at 3e-5 (measured worst: 1.2e-5 over 64 Mi parameters)."""
+    chunk_close(p_got, p_want, s, tol=tol, what=what)
+    tol = UPDATE_TOL
+    pw = np.asarray(p_want, np.float64)
+    u_want = (np.asarray(p_before, np.float64) - pw) / lr
     u_got = (np.asarray(p_before, np.float64) - np.asarray(p_got, np.float64)) / lr
-    chunk_close(u_got, u_want, s, tol=tol, what=what)
+    storage = 2.0 ** -23 * np.abs(pw) / lr
+    excess = np.maximum(np.abs(u_got - u_want) - storage, 0.0)
+    n = len(pw)
+    pad = (-n) % s
+    ex = np.concatenate([excess, np.zeros(pad)]).reshape(-1, s).max(axis=1)
+    sc = np.maximum(np.abs(np.concatenate([u_want, np.zeros(pad)])).reshape(-1, s).max(axis=1), 1e-30)
+    worst = float((ex / sc).max()) if len(ex) else 0.0
+    record(os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], what + " (update)", worst, tol)
+    assert worst <= tol, f"{what}: update error {worst:.3g} of the chunk's largest update (bar {tol:.0e})"
 
 
 def fp16_close(got, want):
@@ -303,8 +326,8 @@ def test_adamw_stage_parity(oracle):
         pw, ew, sw = p_in.copy(), ea_in.copy(), es_in.copy()
         oracle.adamw_apply(pw, ew, sw, step, g.astype(np.float64), want["local_q"], want_q, 0.9, 0.999, 1e-8,
                            0.01, 0.003)
-        chunk_close(host(st.exp_avg), ew, 64, tol=1e-4, what="exp_avg")
-        chunk_close(host(st.exp_avg_sq), sw, 64, tol=1e-4, what="exp_avg_sq")
+        chunk_close(host(st.exp_avg), ew, 64, what="exp_avg")
+        chunk_close(host(st.exp_avg_sq), sw, 64, what="exp_avg_sq")
         update_close(host(params), pw, p_in, 0.003, 64)
 
 
@@ -495,8 +518,8 @@ def test_tc_fused_step_matches_oracle(oracle, monkeypatch, opt_kind, force):
         q = oracle.decode_and_merge(rep, [want["values"]], [want["freq_indices"]], n, 3, 0)
         pw, ew, sw = p0.astype(np.float64), ea0.astype(np.float64), es0.astype(np.float64)
         oracle.adamw_apply(pw, ew, sw, 4, g.astype(np.float64), want["local_q"], q, 0.9, 0.999, 1e-8, 0.0, lr)
-        chunk_close(host(ead), ew, 64, tol=1e-4, what="exp_avg")
-        chunk_close(host(esd), sw, 64, tol=1e-4, what="exp_avg_sq")
+        chunk_close(host(ead), ew, 64, what="exp_avg")
+        chunk_close(host(esd), sw, 64, what="exp_avg_sq")
         update_close(host(pd), pw, p0, lr, 64)
     idx = body[: 4 * want["freq_indices"].size].view(torch.int32).cpu().numpy().astype(np.uint32)
     assert np.array_equal(idx, want["freq_indices"])
@@ -572,8 +595,8 @@ def test_tc_cluster_adamw_prepare_merge_matches_oracle(oracle, monkeypatch, k, f
     q = oracle.decode_and_merge(rep, [w["values"] for w in wants], [w["freq_indices"] for w in wants], n, step, 0)
     pw, ew, sw = p0.astype(np.float64), ea0.astype(np.float64), es0.astype(np.float64)
     oracle.adamw_apply(pw, ew, sw, 4, gs[own].astype(np.float64), wants[own]["local_q"], q, 0.9, 0.999, 1e-8, 0.0, lr)
-    chunk_close(host(ead), ew, 64, tol=1e-4, what="exp_avg")
-    chunk_close(host(esd), sw, 64, tol=1e-4, what="exp_avg_sq")
+    chunk_close(host(ead), ew, 64, what="exp_avg")
+    chunk_close(host(esd), sw, 64, what="exp_avg_sq")
     update_close(host(pd), pw, p0, lr, 64)
 
 
@@ -628,6 +651,6 @@ def test_tc_near_ties_settle_in_fixup(oracle, monkeypatch, sign, dtype):
     q = oracle.decode_and_merge(rep, [want["values"]], [want["freq_indices"]], n, 3, 0)
     pw, ew, sw = p0.astype(np.float64), ea0.astype(np.float64), es0.astype(np.float64)
     oracle.adamw_apply(pw, ew, sw, 4, g.astype(np.float64), want["local_q"], q, 0.9, 0.999, 1e-8, 0.0, lr)
-    chunk_close(host(ead), ew, 64, tol=1e-4, what="exp_avg")
-    chunk_close(host(esd), sw, 64, tol=1e-4, what="exp_avg_sq")
+    chunk_close(host(ead), ew, 64, what="exp_avg")
+    chunk_close(host(esd), sw, 64, what="exp_avg_sq")
     update_close(host(pd), pw, p0, lr, 64)
