@@ -291,7 +291,7 @@ def run_ours(args, rank, world, local_rank):
             return
         # SxR: reduce-scatter in the shard group -> prepare -> NCCL all-gather of the
         # payloads in the replica group -> rank-ordered merge + apply (cluster.cpp:171-232)
-        cluster.step(step, 1e-3, grad, check=False)
+        cluster.step(step, 1e-3, grad)  # status checked every step: a refused step leaves all state as it was
 
     def barrier():
         if distributed:
@@ -345,7 +345,7 @@ def run_ours(args, rank, world, local_rank):
     if distributed:
         # prepare reads g (4); merge+apply reads g again + p/m/v r/w (28) + (1+R) payloads
         P_b = cluster.payload_bytes_per_param  # the exchanged body per parameter (MASK or reference)
-        B_alg = (32 if args.optimizer == "adamw" else 24) + (1 + cluster.topo.nodes) * P_b
+        B_alg = (32 if args.optimizer == "adamw" else 20) + (1 + cluster.topo.nodes) * P_b
     step_ms = ms  # the mean over the timed steps, as ms_per_step
     # dominant kernel: its own launches, timed by events on its stream inside the timed
     # region; the step adds the FP64 fix-up of the uncertified chunks

@@ -11,26 +11,47 @@ torch.distributed (NCCL over NVLink / NVSwitch on a B200 box, gloo on CPU for te
                                            rank-ordered merge on every member
                                            (cluster.cpp:193-231, replicate.cpp:239-314)
 
-The payload of a rank is exactly the reference's serialized body (indices then values
-packed per transfer dtype, replicate.cpp:316-356), so the bytes NCCL moves per rank are
-the reference's wire_bytes; `ledger` records them the way TrafficLedger does
-(cluster.cpp:16-61): intra = reduce-scatter ring bytes, inter = bytes * (R - 1).
+One step runs in three phases (`begin`, `agree`, `commit`; `step` runs all three):
+
+  begin   reduce-scatter, then per bucket (chunk-aligned slices of the shard for DeMo, whose
+          selection is chunk-local, so each bucket's payload is the reference's payload of
+          that sub-vector): the prepare kernel, then the start of the bucket's exchange, which
+          overlaps the prepares of the later buckets;
+  agree   every prepare has latched a non-finite gradient it saw (require_finite,
+          vec.cpp:7-16); the latches are max-reduced over the world on the device, so a bad
+          gradient anywhere refuses the whole step everywhere, as the reference checks every
+          gradient before any state changes (cluster.cpp:182);
+  commit  per bucket: wait for its exchange, the fused merge + apply kernel (a no-op once
+          the step is refused), then the status check.  Momentum (SGD) is double buffered
+          and the host-side step counter restored, so a refused step leaves every state
+          vector as it was (optim.cpp:21).
+
+At R = 1 (S x 1 layouts) there is nothing to exchange and DeMo runs the fused one-pass step
+kernel with double-buffered outputs, swapped when the step succeeds.
+
+The exchange is injectable: `CollectiveExchange` (torch.distributed all-gather, any
+backend), `CopyEngineExchange` (symmetric memory pulled by copy engines over NVLink, NCCL
+only for the agreement), `LocalExchange` (R members in one process on one GPU, tests).  The
+DeMo payload layout per bucket comes from the library before anything runs
+(dmb_plan_exchange): the lossless MASK layout where the tensor-core encoders run, else the
+reference body; every prepare's header is checked against that plan.  `ledger` records the
+bytes the way TrafficLedger does (cluster.cpp:16-61): intra = reduce-scatter ring bytes,
+inter = bytes * (R - 1), beside the reference wire format's bytes for the same exchange.
 """
 from __future__ import annotations
 
 import ctypes as C
 import os
-from dataclasses import dataclass, field
-from typing import Callable, List, Optional
+from dataclasses import dataclass
+from typing import List, Optional
 
 import torch
 import torch.distributed as dist
 
 from . import _capi
-from .core import (OptimizerConfig, OptimizerKind, ReplicatorConfig, Scheme, TransferDtype, _check, _ptr,
-                   _stream,
-                   context, status)
 from ._capi import lib
+from .core import (ConfigError, OptimizerConfig, OptimizerKind, ProtocolError, ReplicatorConfig, Scheme, TrainingError,
+                   _check, _ptr, _stream, context, status)
 
 
 @dataclass
@@ -117,226 +138,366 @@ class ReplicaExchange:
         return [self.gathered[r * self.capacity:(r + 1) * self.capacity] for r in range(self.members)]
 
 
+# ------------------------------------------------------------------ exchanges
+class CollectiveExchange:
+    """torch.distributed all-gather of each bucket's bodies in the replica group (NCCL over
+    NVLink on the GPU box, gloo in the CPU tests); agreement by an all-reduce over `world`."""
+
+    def __init__(self, shard_group, replica_group, world_group=None, members: int = 1, shard_members: int = 1):
+        self.shard_group, self.replica_group, self.world_group = shard_group, replica_group, world_group
+        self.members, self.shard_members = members, shard_members
+
+    def setup(self, xfers: List[int], device) -> None:
+        self.xfers = xfers
+        self.own_slots = [torch.empty(x, dtype=torch.uint8, device=device) for x in xfers]
+        self.gathered = [torch.empty(self.members * x, dtype=torch.uint8, device=device) if self.members > 1 else None
+                         for x in xfers]
+
+    def begin_step(self) -> None:
+        pass
+
+    def own(self, bi: int) -> torch.Tensor:
+        return self.own_slots[bi]
+
+    def reduce_scatter(self, out: torch.Tensor, full: torch.Tensor) -> torch.Tensor:
+        return reduce_scatter_mean(out, full, self.shard_members, self.shard_group)
+
+    def start(self, bi: int):
+        if self.members == 1:
+            return None
+        return dist.all_gather_into_tensor(self.gathered[bi], self.own_slots[bi], group=self.replica_group,
+                                           async_op=True)
+
+    def bodies(self, bi: int, handle) -> List[int]:
+        if self.members == 1:
+            return [self.own_slots[bi].data_ptr()]
+        handle.wait()  # the compute stream waits for the gather; the host does not (NCCL)
+        x = self.xfers[bi]
+        return [self.gathered[bi][r * x:].data_ptr() for r in range(self.members)]
+
+    def agree(self, flag: torch.Tensor) -> None:
+        if self.world_group is not None or dist.is_initialized():
+            if dist.get_world_size(self.world_group) > 1:
+                dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.world_group)
+
+
+class CopyEngineExchange(CollectiveExchange):
+    """The bodies live in symmetric memory (one buffer mapped into every replica-group
+    member, two alternating by step so a member's next prepare never overwrites a body a peer
+    is still copying).  After a device-side barrier each member pulls the others' bodies with
+    cudaMemcpyAsync -- copy engines over NVLink, no SMs -- on a side stream, so the exchange
+    runs under the persistent prepare kernels of the later buckets."""
+
+    def __init__(self, shard_group, replica_group, world_group, members: int, shard_members: int, node: int):
+        super().__init__(shard_group, replica_group, world_group, members, shard_members)
+        self.node = node
+
+    def setup(self, xfers: List[int], device) -> None:
+        import torch.distributed._symmetric_memory as symm
+
+        self.xfers = xfers
+        self.offs, total = [], 0
+        for x in xfers:
+            self.offs.append(total)
+            total += x
+        self.bufs = [symm.empty(total, dtype=torch.uint8, device=device) for _ in range(2)]
+        self.hdls = [symm.rendezvous(b, self.replica_group) for b in self.bufs]
+        if self.hdls[0].world_size != self.members or self.hdls[0].rank != self.node:
+            raise RuntimeError("symmetric-memory rendezvous does not match the replica group")
+        self.gathered = [torch.empty(self.members * x, dtype=torch.uint8, device=device) for x in xfers]
+        self.stream = torch.cuda.Stream(device)
+        self.device = device
+        self.parity = 1
+
+    def begin_step(self) -> None:
+        self.parity ^= 1
+
+    def own(self, bi: int) -> torch.Tensor:
+        o = self.offs[bi]
+        return self.bufs[self.parity][o:o + self.xfers[bi]]
+
+    def start(self, bi: int):
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(self.device))
+        self.stream.wait_event(ready)
+        hdl, x, o = self.hdls[self.parity], self.xfers[bi], self.offs[bi]
+        with torch.cuda.stream(self.stream):
+            hdl.barrier(channel=0)  # every member's prepare of this bucket is done
+            for r in range(self.members):
+                if r != self.node:
+                    self.gathered[bi][r * x:(r + 1) * x].copy_(hdl.get_buffer(r, (x,), torch.uint8, o), non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(self.stream)
+        return done
+
+    def bodies(self, bi: int, handle) -> List[int]:
+        torch.cuda.current_stream(self.device).wait_event(handle)
+        x = self.xfers[bi]
+        return [self.own(bi).data_ptr() if r == self.node else self.gathered[bi][r * x:].data_ptr()
+                for r in range(self.members)]
+
+
+class LocalHub:
+    """R x A members of one cluster in ONE process on one GPU (tests): the members' bodies
+    are read in place, the reduce-scatter is the member-order mean (dmb_grad_mean), and the
+    agreement is the max of the members' flags.  Drive the members phase by phase:
+    hub.grads[rank] = ...; every member.begin(); hub.agree(); every member.commit()."""
+
+    def __init__(self, topo: Topology):
+        self.topo = topo
+        self.members: dict = {}
+        self.grads: dict = {}
+
+    def agree(self) -> None:
+        flags = [m.flag for m in self.members.values()]
+        top = torch.stack(flags).max(dim=0).values
+        for f in flags:
+            f.copy_(top)
+
+
+class LocalExchange(CollectiveExchange):
+    def __init__(self, hub: LocalHub, rank: int):
+        A = hub.topo.accels_per_node
+        super().__init__(None, None, None, hub.topo.nodes, A)
+        self.hub, self.rank = hub, rank
+        self.node, self.accel = divmod(rank, A)
+
+    def setup(self, xfers: List[int], device) -> None:
+        self.xfers = xfers
+        self.own_slots = [torch.empty(x, dtype=torch.uint8, device=device) for x in xfers]
+
+    def reduce_scatter(self, out: torch.Tensor, full: torch.Tensor) -> torch.Tensor:
+        A = self.shard_members
+        if A == 1:
+            out.copy_(full[: out.numel()])
+            return out
+        n = out.numel()
+        ins = [self.hub.grads[self.node * A + a][self.accel * n:(self.accel + 1) * n] for a in range(A)]
+        arr = (C.c_void_p * A)(*[g.data_ptr() for g in ins])
+        _check(lib.dmb_grad_mean(context(out.device).h, arr, A, n, _ptr(out), _stream(out)))
+        return out
+
+    def start(self, bi: int):
+        return None
+
+    def bodies(self, bi: int, handle) -> List[int]:
+        A = self.shard_members
+        return [self.hub.members[n * A + self.accel].exchange.own_slots[bi].data_ptr() for n in range(self.members)]
+
+    def agree(self, flag: torch.Tensor) -> None:
+        pass  # the hub agrees for every member between the phases
+
+
+# ------------------------------------------------------------------ the cluster step
 class HybridCluster:
     """This rank's part of a FlexDeMo cluster step (cluster.cpp:171-232).
 
     Holds the rank's parameter shard and optimizer state on its GPU; `step()` takes the
-    rank's full (padded) gradient, reduce-scatters it inside the node, runs the prepare
-    kernel, all-gathers the payloads across the replica group and applies the merged
-    update with the fused merge + apply kernel.
+    rank's full (padded) gradient, reduce-scatters it inside the node, prepares, exchanges
+    the payloads across the replica group and applies the merged update (see the module
+    docstring for the phases and the failure semantics).
     """
 
     def __init__(self, topo: Topology, param_count: int, opt: OptimizerConfig, rep: ReplicatorConfig,
                  initial_params: torch.Tensor, rank: int, shard_group=None, replica_group=None,
-                 buckets: int = 8, wire: str = "mask"):
+                 buckets: int = 8, wire: str = "mask", exchange=None, world_group=None):
         self.topo, self.opt, self.rep = topo, opt, rep
         self.rank = rank
         self.node, self.accel = divmod(rank, topo.accels_per_node)
         self.param_count = param_count
         self.spec = shard_spec(param_count, topo.accels_per_node, self.accel)
         self.device = initial_params.device
-        self.shard_group, self.replica_group = shard_group, replica_group
+        R, A = topo.nodes, topo.accels_per_node
         L = self.spec.real_len
+        self.sgd = opt.kind == OptimizerKind.DemoSgd
+        self.fused = R == 1 and rep.scheme == Scheme.DeMo and L > 0  # one pass, double-buffered outputs
         self.params = initial_params[self.spec.offset:self.spec.offset + L].clone().contiguous()
-        if opt.kind == OptimizerKind.DemoSgd:
-            self.m = torch.zeros(L, dtype=torch.float32, device=self.device)
+        z = lambda: torch.zeros(L, dtype=torch.float32, device=self.device)  # noqa: E731
+        if self.sgd:
+            self.m, self._m_next = z(), z()
         else:
-            self.exp_avg = torch.zeros(L, dtype=torch.float32, device=self.device)
-            self.exp_avg_sq = torch.zeros(L, dtype=torch.float32, device=self.device)
-        self.steps = C.c_uint64(0)
-        c = rep.c()
-        self.capacity = int(lib.dmb_update_capacity(C.byref(c), L))
-        self.own = torch.empty(self.capacity, dtype=torch.uint8, device=self.device)
-        self.exchange = ReplicaExchange(replica_group, topo.nodes, self.capacity, self.device)
+            self.exp_avg, self.exp_avg_sq = z(), z()
+        if self.fused:  # the fused step writes p (and the moments) into spares, swapped on success
+            self._p_next = z()
+            if not self.sgd:
+                self._ea_next, self._es_next = z(), z()
+        self.steps = 0
         self.shard_grad = torch.empty(self.spec.extent, dtype=torch.float32, device=self.device)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.ledger: List[StepTraffic] = []
-        # Bucketed exchange (DeMo, R > 1): chunk-aligned slices of the shard, each prepared,
-        # all-gathered and merged on its own, so the NVLink transfer of bucket b overlaps the
-        # prepare of b+1 and the merge of b-1.  DeMo's selection is chunk-local, so every
-        # bucket's payload is the reference's body of that sub-vector and the merged result
-        # is the unbucketed one (Random / Striding / DiLoCo / Full use one bucket).
-        # MASK exchange layout (include/demo_b200.h): u64 frequency mask per chunk + values,
-        # lossless, used where the tensor-core AdamW kernels run (s = 64, whole chunks)
-        self.mask_wire = (wire == "mask" and rep.scheme == Scheme.DeMo and opt.kind == OptimizerKind.DecoupledAdamW
-                          and rep.chunk_size == 64 and L % 64 == 0)
-        self.buckets = []
-        if rep.scheme == Scheme.DeMo and topo.nodes > 1 and buckets > 1 and L > 0:
-            tile = 128 * rep.chunk_size
-            edges = sorted({min(L, (L * b // buckets) // tile * tile) for b in range(buckets)} | {L})
-            vbits = 2 if (rep.sign_mode or rep.transfer_dtype == TransferDtype.Ternary) else \
-                (16 if rep.transfer_dtype == TransferDtype.Fp16 else 32)
-            for lo, hi in zip(edges[:-1], edges[1:]):
-                cap = int(lib.dmb_update_capacity(C.byref(c), hi - lo))
-                nch = (hi - lo) // 64
-                body = 24 * nch if vbits == 2 else 8 * nch + (nch * rep.top_k * vbits + 7) // 8  # MASK(_SIGN)
-                xfer = cap if not self.mask_wire else ((body + 15) // 16) * 16
-                self.buckets.append(dict(lo=lo, hi=hi, cap=cap, xfer=xfer,
-                                         own=torch.empty(cap, dtype=torch.uint8, device=self.device),
-                                         gathered=torch.empty(topo.nodes * xfer, dtype=torch.uint8,
-                                                              device=self.device)))
-            self.payload_bytes_per_param = sum(b["xfer"] for b in self.buckets) / L
-        self.ce = self._setup_ce_gather() if self.buckets else None
-
-    def _reduce_scatter(self, grad_full: torch.Tensor) -> torch.Tensor:
-        A = self.topo.accels_per_node
-        if A == 1:
-            return grad_full[: self.spec.extent]
-        return reduce_scatter_mean(self.shard_grad, grad_full, A, self.shard_group)
-
-    def _setup_ce_gather(self):
-        """Copy-engine all-gather over symmetric memory: every member's bucket bodies live in
-        a buffer mapped into all replica-group members; after a device-side barrier each
-        member pulls the others' bodies with cudaMemcpyAsync (copy engines, no SMs), so the
-        exchange overlaps the persistent step kernels.  Two buffers alternate between steps,
-        so a member's next prepare never overwrites a body a peer is still copying.  Falls
-        back to the NCCL all-gather when symmetric memory is unavailable."""
-        if (self.topo.nodes < 2 or os.environ.get("DMB_CE_GATHER", "1") == "0"
-                or dist.get_backend(self.replica_group) != "nccl"):
-            return None
-        try:
-            import torch.distributed._symmetric_memory as symm
-
-            offs, total = [], 0
-            for b in self.buckets:
-                offs.append(total)
-                total += b["xfer"]
-            bufs = [symm.empty(total, dtype=torch.uint8, device=self.device) for _ in range(2)]
-            hdls = [symm.rendezvous(x, self.replica_group) for x in bufs]
-            if hdls[0].world_size != self.topo.nodes or hdls[0].rank != self.node:
-                return None
-            return dict(bufs=bufs, hdls=hdls, offs=offs, stream=torch.cuda.Stream(self.device), step=0)
-        except Exception:  # no symmetric-memory support here: NCCL all-gather
-            return None
-
-    def _step_bucketed(self, step: int, lr: float, g_shard: torch.Tensor, tr: StepTraffic) -> None:
-        R = self.topo.nodes
         ctx = context(self.device).h
-        c, o = self.rep.c(), self.opt.c()
-        st = _stream(g_shard)
-        sgd = self.opt.kind == OptimizerKind.DemoSgd
-        pending = []
-
-        def merge(b, hdr, work):
-            own_ptr = None
-            if isinstance(work, tuple):  # copy-engine gather: (done event, own body)
-                torch.cuda.current_stream(self.device).wait_event(work[0])
-                own_ptr = work[1].data_ptr()
-            else:
-                work.wait()  # the compute stream waits for the gather; the host does not
-            lo, hi = b["lo"], b["hi"]
-            ups = (_capi.Update * R)()
-            for r in range(R):
-                ups[r] = hdr
-                ups[r].body = own_ptr if (own_ptr is not None and r == self.node) else \
-                    b["gathered"][r * b["xfer"]:].data_ptr()
-            if sgd:
-                _check(lib.dmb_merge_apply_sgd(ctx, ups, R, C.byref(c), _ptr(self.params[lo:hi]),
-                                               _ptr(g_shard[lo:hi]), hi - lo, step, float(lr), st))
-            else:
-                _check(lib.dmb_merge_apply_adamw(ctx, ups, R, self.node, C.byref(c), _ptr(self.params[lo:hi]),
-                                                 _ptr(self.exp_avg[lo:hi]), _ptr(self.exp_avg_sq[lo:hi]),
-                                                 C.byref(self.steps_b), _ptr(g_shard[lo:hi]), hi - lo, step,
-                                                 C.byref(o), float(lr), st))
-
-        steps0 = self.steps.value
-        if self.mask_wire:
-            _check(lib.dmb_set_wire_format(ctx, 1))
+        if wire not in ("mask", "reference"):
+            raise ConfigError(f"unknown exchange layout {wire!r}")
+        self.wire = wire
+        # buckets: chunk-aligned slices of the shard (DeMo), one bucket for the other schemes
+        tile = 128 * max(rep.chunk_size, 1)
+        nb = buckets if (rep.scheme == Scheme.DeMo and R > 1) else 1
+        edges = sorted({min(L, (L * b // nb) // tile * tile) for b in range(nb)} | {L})
+        self.buckets = [dict(lo=lo, hi=hi) for lo, hi in zip(edges[:-1], edges[1:])] if L else []
+        # the payload layout of every bucket, from the library, before anything runs
+        c = rep.c()
+        lib.dmb_set_wire_format(ctx, 1 if wire == "mask" else 0)
         try:
-            self._pipeline(step, lr, g_shard, tr, merge, pending, steps0, ctx, c, o, st, sgd, R)
+            for b in self.buckets:
+                h = _capi.Update()
+                _check(lib.dmb_plan_exchange(ctx, C.byref(c), b["hi"] - b["lo"], 0, self.accel, C.byref(h)))
+                b["format"] = int(h.wire_format)
+                b["bytes"] = int(h.bytes)
+                b["xfer"] = max(16, (int(lib.dmb_update_capacity(C.byref(c), b["hi"] - b["lo"])) if not h.wire_format
+                                     else (int(h.bytes) + 15) // 16 * 16))
         finally:
-            if self.mask_wire:
-                lib.dmb_set_wire_format(ctx, 0)
+            lib.dmb_set_wire_format(ctx, 0)
+        self.mask_wire = any(b["format"] for b in self.buckets)
+        self.payload_bytes_per_param = (sum(b["bytes"] for b in self.buckets) / L) if L else 0.0
+        gathered = R * sum(b["xfer"] for b in self.buckets)
+        budget = int(os.environ.get("DMB_GATHER_BUDGET", "0")) or None
+        if budget is not None and gathered > budget:
+            raise ConfigError(f"the step holds {gathered} gathered payload bytes, above DMB_GATHER_BUDGET={budget}")
+        if exchange is None:
+            exchange = self._default_exchange(shard_group, replica_group, world_group)
+        self.exchange = exchange
+        if self.buckets and not self.fused:
+            exchange.setup([b["xfer"] for b in self.buckets], self.device)
+        self.ce = exchange if isinstance(exchange, CopyEngineExchange) else None
+        if isinstance(exchange, LocalExchange):
+            exchange.hub.members[rank] = self
 
-    def _pipeline(self, step, lr, g_shard, tr, merge, pending, steps0, ctx, c, o, st, sgd, R):
-        ce = self.ce
-        if ce is not None:
-            par = ce["step"] & 1
-            ce["step"] += 1
-            cbuf, hdl, cs = ce["bufs"][par], ce["hdls"][par], ce["stream"]
-        for bi, b in enumerate(self.buckets):
-            lo, hi = b["lo"], b["hi"]
-            hdr = _capi.Update()
-            own = cbuf[ce["offs"][bi]: ce["offs"][bi] + b["xfer"]] if ce is not None else b["own"]
-            hdr.body = own.data_ptr()
-            if sgd:
-                _check(lib.dmb_demo_sgd_prepare(ctx, _ptr(g_shard[lo:hi]), _ptr(self.m[lo:hi]), _ptr(self.m[lo:hi]),
-                                                hi - lo, C.byref(o), C.byref(c), step, self.accel, C.byref(hdr),
-                                                None, None, st))
-            else:
-                _check(lib.dmb_adamw_prepare(ctx, _ptr(g_shard[lo:hi]), hi - lo, C.byref(c), step, self.accel,
-                                             C.byref(hdr), None, st))
-            tr.inter_bytes += int(hdr.bytes) * (R - 1)
-            tr.inter_bytes_reference += int(lib.dmb_wire_bytes(hdr.n_values, hdr.n_indices,
-                                                                self.rep.transfer_dtype)) * (R - 1)
-            if ce is not None:
-                ready = torch.cuda.Event()
-                ready.record(torch.cuda.current_stream(self.device))
-                cs.wait_event(ready)
-                with torch.cuda.stream(cs):
-                    hdl.barrier(channel=0)  # every member's prepare of this bucket is done
-                    for r in range(R):
-                        if r != self.node:
-                            b["gathered"][r * b["xfer"]:(r + 1) * b["xfer"]].copy_(
-                                hdl.get_buffer(r, (b["xfer"],), torch.uint8, ce["offs"][bi]), non_blocking=True)
-                    done = torch.cuda.Event()
-                    done.record(cs)
-                work = (done, own)
-            else:
-                work = dist.all_gather_into_tensor(b["gathered"], b["own"][: b["xfer"]], group=self.replica_group,
-                                                   async_op=True)
-            if pending:
-                self.steps_b = C.c_uint64(steps0)
-                merge(*pending.pop())
-            pending.append((b, hdr, work))
-        self.steps_b = C.c_uint64(steps0)
-        merge(*pending.pop())
-        self.steps = self.steps_b  # every bucket advanced the AdamW counter from the same value
+    def _default_exchange(self, shard_group, replica_group, world_group):
+        R, A = self.topo.nodes, self.topo.accels_per_node
+        if (R > 1 and os.environ.get("DMB_CE_GATHER", "1") != "0" and replica_group is not None
+                and dist.get_backend(replica_group) == "nccl"):
+            try:
+                return CopyEngineExchange(shard_group, replica_group, world_group, R, A, self.node)
+            except Exception:  # no symmetric-memory support: the NCCL all-gather
+                pass
+        return CollectiveExchange(shard_group, replica_group, world_group, R, A)
+
+    # ---- phases -----------------------------------------------------------------
+    def begin(self, step: int, lr: float, grad_full: torch.Tensor) -> None:
+        """reduce-scatter, every bucket's prepare and the start of its exchange"""
+        topo, L = self.topo, self.spec.real_len
+        A, R = topo.accels_per_node, topo.nodes
+        tr = StepTraffic(step=step, reduce_scatter_events=1, synchronize_events=1)
+        tr.intra_bytes = A * (A - 1) * self.spec.extent * 4  # ring model, cluster.cpp:87
+        self._tr, self._step, self._lr = tr, step, float(lr)
+        self._steps0 = self.steps
+        # the pad tail never leaves the node (cluster.cpp:201)
+        self.g_shard = grad_full[:L] if A == 1 else self.exchange.reduce_scatter(self.shard_grad, grad_full)[:L]
+        self._pending = []
+        if not L:
+            return
+        ctx = context(self.device).h
+        st = _stream(self.g_shard)
+        c, o = self.rep.c(), self.opt.c()
+        if self.fused:
+            self._fused(ctx, c, o, st)
+        else:
+            self.exchange.begin_step()
+            lib.dmb_set_wire_format(ctx, 1 if self.wire == "mask" else 0)
+            try:
+                for bi, b in enumerate(self.buckets):
+                    lo, hi = b["lo"], b["hi"]
+                    hdr = _capi.Update()
+                    hdr.body = self.exchange.own(bi).data_ptr()
+                    if self.sgd:
+                        _check(lib.dmb_demo_sgd_prepare(ctx, _ptr(self.g_shard[lo:hi]), _ptr(self.m[lo:hi]),
+                                                        _ptr(self._m_next[lo:hi]), hi - lo, C.byref(o), C.byref(c),
+                                                        step, self.accel, C.byref(hdr), None, None, st))
+                    else:
+                        _check(lib.dmb_adamw_prepare(ctx, _ptr(self.g_shard[lo:hi]), hi - lo, C.byref(c), step,
+                                                     self.accel, C.byref(hdr), None, st))
+                    if not hdr.empty and (int(hdr.wire_format) != b["format"] or int(hdr.bytes) > b["xfer"]):
+                        raise ProtocolError(f"bucket {bi}: the prepare produced layout {hdr.wire_format} / "
+                                            f"{hdr.bytes} B, planned {b['format']} / {b['xfer']} B")
+                    tr.inter_bytes += int(hdr.bytes) * (R - 1)  # cluster.cpp:212
+                    tr.inter_bytes_reference += int(lib.dmb_wire_bytes(hdr.n_values, hdr.n_indices,
+                                                                        self.rep.transfer_dtype)) * (R - 1)
+                    handle = self.exchange.start(bi) if not hdr.empty else None
+                    self._pending.append((b, hdr, handle))
+            finally:
+                lib.dmb_set_wire_format(ctx, 0)
+        _check(lib.dmb_latch_export(ctx, _ptr(self.flag), st))
+
+    def agree(self) -> None:
+        self.exchange.agree(self.flag)
+
+    def commit(self, check: bool = True) -> StepTraffic:
+        """merges + applies (no-ops on a refused step), status, buffer swaps"""
+        tr, step, lr = self._tr, self._step, self._lr
+        L = self.spec.real_len
+        if L:
+            ctx = context(self.device).h
+            st = _stream(self.g_shard)
+            _check(lib.dmb_latch_import(ctx, _ptr(self.flag), st))
+            if not self.fused:
+                c, o = self.rep.c(), self.opt.c()
+                R = self.topo.nodes
+                steps = C.c_uint64(self.steps)
+                for bi, (b, hdr, handle) in enumerate(self._pending):
+                    lo, hi = b["lo"], b["hi"]
+                    ups, n_up = None, 0
+                    if not hdr.empty:
+                        ptrs = self.exchange.bodies(bi, handle)
+                        ups = (_capi.Update * R)()
+                        for r in range(R):
+                            ups[r] = hdr
+                            ups[r].body = ptrs[r]
+                        n_up = R
+                    if self.sgd:
+                        _check(lib.dmb_merge_apply_sgd(ctx, ups, n_up, C.byref(c), _ptr(self.params[lo:hi]),
+                                                       _ptr(self.g_shard[lo:hi]), hi - lo, step, lr, st))
+                    else:
+                        steps = C.c_uint64(self._steps0)  # every bucket advances the counter from the same value
+                        _check(lib.dmb_merge_apply_adamw(ctx, ups, n_up, self.node, C.byref(c),
+                                                         _ptr(self.params[lo:hi]), _ptr(self.exp_avg[lo:hi]),
+                                                         _ptr(self.exp_avg_sq[lo:hi]), C.byref(steps),
+                                                         _ptr(self.g_shard[lo:hi]), hi - lo, step, C.byref(o), lr, st))
+                self.steps = self._steps0 + 1 if not self.sgd else self.steps
+        self._swap()
+        self._pending = []
+        self.ledger.append(tr)
+        if check:
+            self.status()
+        return tr
 
     def step(self, step: int, lr: float, grad_full: torch.Tensor, check: bool = True) -> StepTraffic:
-        topo = self.topo
-        L = self.spec.real_len
-        tr = StepTraffic(step=step)
-        g_shard = self._reduce_scatter(grad_full)[:L]  # the pad tail never leaves the node (:201)
-        A = topo.accels_per_node
-        tr.intra_bytes = A * (A - 1) * self.spec.extent * 4  # ring model, cluster.cpp:87
-        tr.reduce_scatter_events = 1
-        if self.buckets:
-            tr.synchronize_events = 1
-            self._step_bucketed(step, lr, g_shard, tr)
-            if check:
-                status(self.device)
-            self.ledger.append(tr)
-            return tr
-        ctx = context(self.device).h
-        st = _stream(g_shard)
-        c, o = self.rep.c(), self.opt.c()
-        hdr = _capi.Update()
-        hdr.body = self.own.data_ptr()
-        if self.opt.kind == OptimizerKind.DemoSgd:
-            _check(lib.dmb_demo_sgd_prepare(ctx, _ptr(g_shard), _ptr(self.m), _ptr(self.m), L, C.byref(o),
-                                            C.byref(c), step, self.accel, C.byref(hdr), None, None, st))
-        else:
-            _check(lib.dmb_adamw_prepare(ctx, _ptr(g_shard), L, C.byref(c), step, self.accel, C.byref(hdr),
-                                         None, st))
-        tr.inter_bytes = int(hdr.bytes) * (topo.nodes - 1)  # cluster.cpp:212
-        tr.synchronize_events = 1
-        R = topo.nodes
-        ups = (_capi.Update * R)()
-        if not hdr.empty:
-            bodies = self.exchange.gather(self.own)
-            for r in range(R):
-                ups[r] = hdr
-                ups[r].body = bodies[r].data_ptr()
-        n_up = 0 if hdr.empty else R
-        if self.opt.kind == OptimizerKind.DemoSgd:
-            _check(lib.dmb_merge_apply_sgd(ctx, ups if n_up else None, n_up, C.byref(c), _ptr(self.params),
-                                           _ptr(g_shard), L, step, float(lr), st))
-        else:
-            _check(lib.dmb_merge_apply_adamw(ctx, ups if n_up else None, n_up, self.node, C.byref(c),
-                                             _ptr(self.params), _ptr(self.exp_avg), _ptr(self.exp_avg_sq),
-                                             C.byref(self.steps), _ptr(g_shard), L, step, C.byref(o), float(lr),
-                                             st))
-        if check:
+        self.begin(step, lr, grad_full)
+        self.agree()
+        return self.commit(check)
+
+    def status(self) -> None:
+        """Synchronize; on a refused step undo the buffer swaps and the step counter, then
+        raise TrainingError (every state vector is as before the step)."""
+        try:
             status(self.device)
-        self.ledger.append(tr)
-        return tr
+        except TrainingError:
+            self._swap()  # back to the buffers of the last good step
+            self.steps = self._steps0
+            raise
+
+    # ---- internals ----------------------------------------------------------------
+    def _swap(self) -> None:
+        if not self.spec.real_len:
+            return
+        if self.sgd:
+            self.m, self._m_next = self._m_next, self.m
+        if self.fused:
+            self.params, self._p_next = self._p_next, self.params
+            if not self.sgd:
+                self.exp_avg, self._ea_next = self._ea_next, self.exp_avg
+                self.exp_avg_sq, self._es_next = self._es_next, self.exp_avg_sq
+
+    def _fused(self, ctx, c, o, st) -> None:
+        """R = 1: prepare -> merge(R = 1) -> apply in one pass (dmb_step_*_local) into the spares"""
+        L, step, lr = self.spec.real_len, self._step, self._lr
+        if self.sgd:
+            _check(lib.dmb_step_sgd_local(ctx, _ptr(self.g_shard), _ptr(self.m), _ptr(self._m_next),
+                                          _ptr(self.params), _ptr(self._p_next), L, C.byref(o), C.byref(c), step,
+                                          self.accel, lr, None, st))
+        else:
+            steps = C.c_uint64(self.steps)
+            _check(lib.dmb_step_adamw_local(ctx, _ptr(self.g_shard), _ptr(self.params), _ptr(self._p_next),
+                                            _ptr(self.exp_avg), _ptr(self._ea_next), _ptr(self.exp_avg_sq),
+                                            _ptr(self._es_next), C.byref(steps), L, C.byref(o), C.byref(c), step,
+                                            self.accel, lr, None, st))
+            self.steps = int(steps.value)

@@ -386,6 +386,17 @@ int ensure_random(dmb_ctx* ctx, const dmb_rep_cfg* cfg, uint64_t step, uint32_t 
     r.capacity = len;
     ctx->rnd_len_cap = len;
   }
+  RandomScratch& r = ctx->rnd;
+  const uint64_t blocks = (len + kMtBlockOutputs - 1) / kMtBlockOutputs;
+  if (!r.mt_seq) {
+    DMB_CUDA_TRY(cudaMalloc(&r.mt_seq, kMtSeqWords * 8));
+    DMB_CUDA_TRY(cudaMalloc(&r.mt_reject, sizeof(unsigned long long)));
+  }
+  if (blocks > r.mt_blocks_cap) {
+    cudaFree(r.mt_windows);
+    DMB_CUDA_TRY(cudaMalloc(&r.mt_windows, blocks * 312 * 8));
+    r.mt_blocks_cap = blocks;
+  }
   // Rng(mix_seed(seed, step, shard)) seeds the engine with mix_seed(.) once more
   // (rng.hpp:21, replicate.cpp:167).
   auto mix64 = [](uint64_t z) {
@@ -395,7 +406,9 @@ int ensure_random(dmb_ctx* ctx, const dmb_rep_cfg* cfg, uint64_t step, uint32_t 
     return z ^ (z >> 31);
   };
   const uint64_t derived = mix64(mix64(mix64(cfg->seed) ^ step) ^ (uint64_t)shard);
-  launch_random_indices(mix64(derived), len, count, ctx->rnd, st);
+  const char* err = nullptr;
+  if (launch_random_indices(mix64(derived), len, count, ctx->rnd, st, &err) != DMB_OK)
+    return fail(DMB_CUDA, "random index set: %s", err ? err : "?");
   if (int rc = last_launch()) return rc;
   ctx->rnd_key = key;
   return DMB_OK;
@@ -608,6 +621,9 @@ int dmb_ctx_destroy(dmb_ctx* ctx) {
   cudaFree(r.bitmap);
   cudaFree(r.rank);
   cudaFree(r.idx);
+  cudaFree(r.mt_seq);
+  cudaFree(r.mt_windows);
+  cudaFree(r.mt_reject);
   cudaFree(ctx->status);
   cudaFree(ctx->aux);
   delete ctx;
@@ -1044,6 +1060,14 @@ int dmb_fallback_chunks(dmb_ctx* ctx, void* stream, uint64_t* count) {
   DMB_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
   *count = a.fallback_chunks + b.fallback_chunks;
   return DMB_OK;
+}
+
+// test hook (not in the public header): the MT19937-64 jump-ahead of substream b, on the host
+int dmb_debug_mt_jump_check(uint64_t engine_seed, uint64_t b) {
+  const char* err = nullptr;
+  const int rc = mt_jump_check(engine_seed, b, &err);
+  if (rc < 0) return fail(DMB_CUDA, "%s", err ? err : "jump table");
+  return rc;
 }
 
 // tuning hook (not in the public header): device buffer of 32 x 16 u64 timestamps

@@ -231,10 +231,20 @@ struct RandomScratch {
   uint32_t* bitmap;  // selected values, 1 bit each
   uint32_t* rank;    // exclusive prefix popcount per 32-bit word
   uint32_t* idx;     // sorted selected indices
-  int* fixup;        // rejection fix-up flag
   uint64_t capacity; // elements
+  // MT19937-64 substreams (random_index.cu): the engine's first words, the start window of
+  // every block of kMtBlockOutputs outputs, the first output a Lemire rejection may touch
+  uint64_t* mt_seq;
+  uint64_t* mt_windows;
+  uint64_t mt_blocks_cap;
+  unsigned long long* mt_reject;
 };
-void launch_random_indices(uint64_t engine_seed, uint64_t len, uint64_t count,
-                           const RandomScratch& s, cudaStream_t stream);
+constexpr uint64_t kMtBlockOutputs = 312ull * 128ull;  // engine outputs per substream
+constexpr uint64_t kMtSeqWords = 312ull * 65ull;       // seeded words + 64 twists (>= 19937 + 312)
+// returns DMB_OK or DMB_CUDA (message in *err)
+int launch_random_indices(uint64_t engine_seed, uint64_t len, uint64_t count, const RandomScratch& s,
+                          cudaStream_t stream, const char** err);
+// host-only check of the substream jump-ahead (tests): 0 when substream b's start window is exact
+int mt_jump_check(uint64_t engine_seed, uint64_t b, const char** err);
 
 }  // namespace dmb

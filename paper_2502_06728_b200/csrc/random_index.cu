@@ -7,15 +7,37 @@
 //
 // Only the iterations i = L .. count+1 decide WHICH values end in positions
 // [0, count); the later ones permute that prefix among itself and the result is
-// sorted anyway.  So (1) one CTA draws j_i for those L - count iterations from the
-// MT19937-64 stream (block-parallel twist, Lemire debias with an exact sequential
-// fix-up when a rejection occurs); (2) for every position t, first[t]/second[t]
+// sorted anyway.  So (1) the draws j_i of those L - count iterations come from the
+// MT19937-64 stream split into substreams of kMtBlockOutputs outputs, one CTA each, every
+// substream started by a GF(2) jump-ahead (below); Lemire's debias rejects an output with
+// probability < 2^-32, and a rejection shifts every later draw by one output, so the CTAs
+// assume none and report the first output that could be one -- an exact sequential
+// replay from that substream fixes the rare case; (2) for every position t, first[t]/second[t]
 // hold the two smallest iterations that targeted it (atomicMin passes); (3) the
 // value that ends in position x < count is resolved by following
 //   D(i) = value at position i-1 just before iteration i
 //        = D(min{i' > i : j_i' = i-1})  or  i-1 if there is none
 // from i* = first[x]; (4) selected values are marked in a bitmap and compacted in
-// ascending order (no sort).  Nothing here runs on the host.
+// ascending order (no sort).
+//
+// Jump-ahead.  One engine output advances the state window (x_i .. x_i+311) by one word:
+// a linear map T over GF(2) whose characteristic polynomial phi (degree 19937) is found once
+// per process by Berlekamp-Massey on the engine's own output bits.  With
+// P_b(x) = x^(b W) mod phi (seed independent, computed once on the host and cached), the
+// window at output b W is  P_b(T) s0 = XOR over the set coefficients i of P_b of the window
+// (x_i .. x_i+311)  -- a correlation of P_b's bits with the first 20 k words of the seeded
+// engine, which one CTA computes in shared memory.  It differs from T^(bW) s0 at most in
+// the 31 low bits of the window's first word, which the twist never reads (only its upper
+// 33 bits enter y), so every output of the substream is exact.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
 #include "dmb_internal.cuh"
 
 namespace dmb {
@@ -24,8 +46,9 @@ namespace {
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr int kMtN = 312;
 constexpr int kMtThreads = 320;
+constexpr uint64_t kMtTwists = kMtBlockOutputs / kMtN;  // twists per substream
 
-__device__ __forceinline__ uint64_t temper(uint64_t y) {
+__host__ __device__ __forceinline__ uint64_t temper(uint64_t y) {
   y ^= (y >> 29) & 0x5555555555555555ULL;
   y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
   y ^= (y << 37) & 0xFFF7EEE000000000ULL;
@@ -33,89 +56,341 @@ __device__ __forceinline__ uint64_t temper(uint64_t y) {
   return y;
 }
 
-__device__ __forceinline__ uint64_t twist_word(uint64_t cur, uint64_t next, uint64_t far) {
+__host__ __device__ __forceinline__ uint64_t twist_word(uint64_t cur, uint64_t next, uint64_t far) {
   const uint64_t y = (cur & 0xFFFFFFFF80000000ULL) | (next & 0x7FFFFFFFULL);
   return far ^ (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
 }
 
-// draws[d] = below(len - d) for d in [0, ndraws), consuming the engine in order.
-__global__ void __launch_bounds__(kMtThreads) mt_draws_kernel(uint64_t engine_seed, uint64_t len,
-                                                              uint64_t ndraws,
-                                                              uint32_t* __restrict__ draws) {
+// one in-place twist of the 312-word window by kMtThreads threads (two dependent halves)
+__device__ __forceinline__ void twist_block(uint64_t* mt, int t) {
+  uint64_t nv = 0;
+  if (t < 156) nv = twist_word(mt[t], mt[t + 1], mt[t + 156]);
+  __syncthreads();
+  if (t < 156) mt[t] = nv;
+  __syncthreads();
+  if (t >= 156 && t < 311) nv = twist_word(mt[t], mt[t + 1], mt[t - 156]);
+  __syncthreads();
+  if (t >= 156 && t < 311) mt[t] = nv;
+  __syncthreads();
+  if (t == 0) mt[311] = twist_word(mt[311], mt[0], mt[155]);
+  __syncthreads();
+}
+
+// std::mt19937_64 seeding (f = 6364136223846793005), then the first 64 twists: seq holds the
+// words x_0 .. x_{kMtSeqWords-1} of the engine (the window at output i is seq[i .. i+311])
+__global__ void __launch_bounds__(kMtThreads) mt_seq_kernel(uint64_t engine_seed, uint64_t* __restrict__ seq) {
   __shared__ uint64_t mt[kMtN];
-  __shared__ int any_reject;
-  __shared__ uint64_t d_shared;
   const int t = threadIdx.x;
   if (t == 0) {
-    // std::mt19937_64 seeding (f = 6364136223846793005)
     uint64_t v = engine_seed;
     mt[0] = v;
     for (int i = 1; i < kMtN; ++i) {
       v = 6364136223846793005ULL * (v ^ (v >> 62)) + (uint64_t)i;
       mt[i] = v;
     }
-    d_shared = 0;
   }
   __syncthreads();
-  uint64_t d0 = 0;
-  while (d0 < ndraws) {
-    // ---- twist: k < 156 from old words, 156 <= k < 311 from new, then k = 311 ----
-    uint64_t nv = 0;
-    if (t < 156) nv = twist_word(mt[t], mt[t + 1], mt[t + 156]);
+  if (t < kMtN) seq[t] = mt[t];
+  for (uint64_t tw = 1; tw * kMtN < kMtSeqWords; ++tw) {
+    twist_block(mt, t);
+    if (t < kMtN) seq[tw * kMtN + t] = mt[t];
+  }
+}
+
+// Lemire below(n) on output x: the draw, and whether the output could be rejected
+__device__ __forceinline__ uint32_t lemire(uint64_t x, uint64_t n, bool& rejected) {
+  const uint64_t lo = x * n;
+  rejected = lo < n && lo < (0ULL - n) % n;  // the threshold (2^64 - n) mod n is < n
+  return (uint32_t)__umul64hi(x, n);
+}
+
+// Substream b: window P_b(T) s0 by correlation, then kMtTwists twists; draw d = output o
+// (no rejection before o assumed; the first possible rejection is reported in *reject)
+__global__ void __launch_bounds__(kMtThreads) mt_block_kernel(const uint64_t* __restrict__ seq,
+                                                              const uint64_t* __restrict__ polys, uint64_t len,
+                                                              uint64_t ndraws, uint32_t* __restrict__ draws,
+                                                              uint64_t* __restrict__ windows,
+                                                              unsigned long long* __restrict__ reject) {
+  extern __shared__ uint64_t sm[];
+  uint64_t* xs = sm;                   // the engine's first kMtSeqWords words
+  uint64_t* poly = xs + kMtSeqWords;   // P_b, bit i = coefficient of x^i
+  uint64_t* mt = poly + kMtN;          // the substream's window
+  const int t = threadIdx.x;
+  const uint64_t b = blockIdx.x;
+  if (b == 0) {
+    if (t < kMtN) mt[t] = seq[t];
+  } else {
+    for (uint64_t i = t; i < kMtSeqWords; i += kMtThreads) xs[i] = seq[i];
+    if (t < kMtN) poly[t] = polys[b * kMtN + t];
     __syncthreads();
-    if (t < 156) mt[t] = nv;
-    __syncthreads();
-    if (t >= 156 && t < 311) nv = twist_word(mt[t], mt[t + 1], mt[t - 156]);
-    __syncthreads();
-    if (t >= 156 && t < 311) mt[t] = nv;
-    __syncthreads();
-    if (t == 0) {
-      mt[311] = twist_word(mt[311], mt[0], mt[155]);
-      any_reject = 0;
-    }
-    __syncthreads();
-    // ---- Lemire below(n), n = len - d: accept unless low64(x*n) < (2^64 - n) % n ----
-    uint64_t x = 0;
-    uint32_t hi = 0;
-    bool mine = false;
     if (t < kMtN) {
-      x = temper(mt[t]);
-      const uint64_t d = d0 + t;
-      if (d < ndraws) {
-        mine = true;
-        const uint64_t n = len - d;
-        const uint64_t lo = x * n;
-        hi = (uint32_t)__umul64hi(x, n);
-        if (lo < n) {  // the threshold is < n: only then can it reject
-          const uint64_t threshold = (0ULL - n) % n;
-          if (lo < threshold) any_reject = 1;
+      uint64_t acc = 0;
+      for (int w = 0; w < kMtN; ++w) {  // uniform across the CTA: no divergence
+        uint64_t bits = poly[w];
+        while (bits) {
+          const int i = 64 * w + __ffsll((long long)bits) - 1;
+          bits &= bits - 1;
+          acc ^= xs[i + t];
         }
       }
+      mt[t] = acc;
+    }
+  }
+  __syncthreads();
+  if (t < kMtN) windows[b * kMtN + t] = mt[t];
+  const uint64_t o0 = b * kMtBlockOutputs;
+  for (uint64_t tw = 0; tw < kMtTwists && o0 + tw * kMtN < ndraws; ++tw) {
+    twist_block(mt, t);
+    const uint64_t o = o0 + tw * kMtN + t;
+    if (t < kMtN && o < ndraws) {
+      bool rej;
+      draws[o] = lemire(temper(mt[t]), len - o, rej);
+      if (rej) atomicMin(reject, (unsigned long long)o);
+    }
+  }
+}
+
+// The rare case: an output from *reject on was rejected, so every later draw moves by one
+// output.  Replay from the start of that substream, sequentially from the rejection on.
+__global__ void __launch_bounds__(kMtThreads) mt_fixup_kernel(const uint64_t* __restrict__ windows, uint64_t len,
+                                                              uint64_t ndraws, uint32_t* __restrict__ draws,
+                                                              const unsigned long long* __restrict__ reject) {
+  __shared__ uint64_t mt[kMtN];
+  __shared__ uint64_t d_shared;
+  const uint64_t ostar = *reject;
+  if (ostar >= ndraws) return;
+  const int t = threadIdx.x;
+  const uint64_t b = ostar / kMtBlockOutputs;
+  if (t < kMtN) mt[t] = windows[b * kMtN + t];
+  uint64_t o = b * kMtBlockOutputs, d = o;  // no rejection before ostar: draw = output there
+  if (t == 0) d_shared = d;
+  __syncthreads();
+  while (d < ndraws) {
+    twist_block(mt, t);
+    if (t == 0) {
+      for (int q = 0; q < kMtN && d < ndraws; ++q, ++o) {
+        if (o < ostar) {  // unaffected: already written by mt_block_kernel
+          ++d;
+          continue;
+        }
+        bool rej;
+        const uint32_t v = lemire(temper(mt[q]), len - d, rej);
+        if (rej) continue;  // consumed without a draw
+        draws[d++] = v;
+      }
+      d_shared = d;
     }
     __syncthreads();
-    if (!any_reject) {
-      if (mine) draws[d0 + t] = hi;
-      d0 += kMtN;
-    } else {
-      // exact sequential replay of this batch: a rejection consumes an output
-      // without producing a draw, shifting every later draw by one
-      if (t == 0) {
-        uint64_t d = d0;
-        for (int q = 0; q < kMtN && d < ndraws; ++q) {
-          const uint64_t xx = temper(mt[q]);
-          const uint64_t n = len - d;
-          const uint64_t lo = xx * n;
-          if (lo < n && lo < (0ULL - n) % n) continue;
-          draws[d] = (uint32_t)__umul64hi(xx, n);
-          ++d;
-        }
-        d_shared = d;
-      }
-      __syncthreads();
-      d0 = d_shared;
-    }
+    d = d_shared;  // o advances in thread 0 only; the loop condition uses d
     __syncthreads();
   }
+}
+
+// ---- host: GF(2)[x] arithmetic for the jump polynomials ----
+constexpr int kDeg = 19937;
+constexpr int kPW = kMtN;  // words of a reduced polynomial (degree < 19937)
+
+struct JumpTable {
+  std::mutex mu;
+  bool ready = false;
+  std::vector<uint64_t> phish;                 // 64 x (kPW + 1) words: phi << s, s = 0..63
+  std::vector<std::vector<uint64_t>> polys;    // x^(b W) mod phi, b = 0, 1, ...
+  std::map<int, std::pair<uint64_t*, uint64_t>> dev;  // device copies (pointer, polys held)
+  std::string error;
+};
+JumpTable& jump_table() {
+  static JumpTable t;
+  return t;
+}
+
+inline int bit(const std::vector<uint64_t>& v, uint64_t i) { return (int)((v[i >> 6] >> (i & 63)) & 1u); }
+
+// reduce a product (up to degree 2 * 19936) modulo phi in place; result in words [0, kPW)
+void reduce(std::vector<uint64_t>& p, const std::vector<uint64_t>& phish) {
+  for (int64_t k = (int64_t)p.size() * 64 - 1; k >= kDeg; --k) {
+    if (!((p[k >> 6] >> (k & 63)) & 1u)) continue;
+    const uint64_t sh = (uint64_t)(k - kDeg);
+    const uint64_t w = sh >> 6, s = sh & 63;
+    const uint64_t* ph = &phish[s * (kPW + 1)];
+    for (int q = 0; q <= kPW && w + q < p.size(); ++q) p[w + q] ^= ph[q];
+  }
+  p.resize(kPW);
+}
+
+std::vector<uint64_t> mulmod(const std::vector<uint64_t>& a, const std::vector<uint64_t>& b,
+                             const std::vector<uint64_t>& phish) {
+  std::vector<uint64_t> bsh((size_t)64 * (kPW + 1));  // b << s
+  for (int s = 0; s < 64; ++s)
+    for (int q = 0; q <= kPW; ++q) {
+      const uint64_t lo = q < kPW ? b[q] << s : 0;
+      const uint64_t hi = (q > 0 && s) ? b[q - 1] >> (64 - s) : 0;
+      bsh[(size_t)s * (kPW + 1) + q] = lo | hi;
+    }
+  std::vector<uint64_t> p(2 * kPW + 2, 0);
+  for (int w = 0; w < kPW; ++w) {
+    uint64_t bits = a[w];
+    while (bits) {
+      const int s = __builtin_ctzll(bits);
+      bits &= bits - 1;
+      const uint64_t* src = &bsh[(size_t)s * (kPW + 1)];
+      for (int q = 0; q <= kPW; ++q) p[w + q] ^= src[q];
+    }
+  }
+  reduce(p, phish);
+  return p;
+}
+
+std::vector<uint64_t> sqrmod(const std::vector<uint64_t>& a, const std::vector<uint64_t>& phish) {
+  auto spread = [](uint32_t x) {  // bit i -> bit 2i
+    uint64_t v = x;
+    v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+    v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+    v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+    v = (v | (v << 2)) & 0x3333333333333333ull;
+    v = (v | (v << 1)) & 0x5555555555555555ull;
+    return v;
+  };
+  std::vector<uint64_t> p(2 * kPW + 2, 0);
+  for (int w = 0; w < kPW; ++w) {
+    p[2 * w] = spread((uint32_t)a[w]);
+    p[2 * w + 1] = spread((uint32_t)(a[w] >> 32));
+  }
+  reduce(p, phish);
+  return p;
+}
+
+std::vector<uint64_t> powmod(std::vector<uint64_t> base, uint64_t e, const std::vector<uint64_t>& phish) {
+  std::vector<uint64_t> r(kPW, 0);
+  r[0] = 1;
+  while (e) {
+    if (e & 1) r = mulmod(r, base, phish);
+    e >>= 1;
+    if (e) base = sqrmod(base, phish);
+  }
+  return r;
+}
+
+// phi by Berlekamp-Massey on the most significant bit of the engine's words x_312, x_313, ...
+bool build_phi(JumpTable& J) {
+  const int N = 2 * kDeg + 64;
+  std::vector<uint64_t> mt(kMtN);
+  uint64_t v = 5489;
+  mt[0] = v;
+  for (int i = 1; i < kMtN; ++i) {
+    v = 6364136223846793005ULL * (v ^ (v >> 62)) + (uint64_t)i;
+    mt[i] = v;
+  }
+  std::vector<uint8_t> s(N);
+  for (int n = 0, pos = kMtN; n < N; ++n, ++pos) {
+    if (pos == kMtN) {
+      for (int k = 0; k < kMtN; ++k) mt[k] = twist_word(mt[k], mt[(k + 1) % kMtN], mt[(k + 156) % kMtN]);
+      pos = 0;
+    }
+    s[n] = (uint8_t)(mt[pos] >> 63);
+  }
+  const int W = N / 64 + 2;
+  std::vector<uint64_t> R(W + 2, 0), Cp(W + 2, 0), Bp(W + 2, 0), T;
+  for (int t = 0; t < N; ++t)  // R[t] = s[N - 1 - t]
+    if (s[N - 1 - t]) R[t >> 6] |= 1ull << (t & 63);
+  Cp[0] = Bp[0] = 1;
+  int L = 0, m = 1;
+  auto window = [&](uint64_t off) {  // 64 bits of R from bit off
+    const uint64_t w = off >> 6, sh = off & 63;
+    const uint64_t lo = w < R.size() ? R[w] : 0, hi = w + 1 < R.size() ? R[w + 1] : 0;
+    return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+  };
+  for (int n = 0; n < N; ++n) {
+    const uint64_t off = (uint64_t)(N - 1 - n);  // R[off + i] = s[n - i]
+    uint64_t acc = 0;
+    for (int w = 0; w <= L / 64; ++w) acc ^= Cp[w] & window(off + 64ull * w);
+    // C has no bits above degree L, so the words up to L / 64 hold the whole sum
+    const int d = __builtin_parityll(acc);
+    if (!d) {
+      ++m;
+      continue;
+    }
+    const bool grow = 2 * L <= n;
+    if (grow) T = Cp;
+    const int ws = m >> 6, bs = m & 63;
+    for (int q = W + 1; q >= 0; --q) {
+      const uint64_t lo = q - ws >= 0 ? Bp[q - ws] << bs : 0;
+      const uint64_t hi = (bs && q - ws - 1 >= 0) ? Bp[q - ws - 1] >> (64 - bs) : 0;
+      Cp[q] ^= lo | hi;
+    }
+    if (grow) {
+      L = n + 1 - L;
+      Bp = T;
+      m = 1;
+    } else {
+      ++m;
+    }
+  }
+  if (L != kDeg) {
+    J.error = "Berlekamp-Massey found a recurrence of degree " + std::to_string(L) + ", not 19937";
+    return false;
+  }
+  // phi(x) = x^L C(1/x): coefficient j of phi is C_{L - j}
+  std::vector<uint64_t> phi(kPW + 1, 0);
+  for (int j = 0; j <= kDeg; ++j)
+    if (bit(Cp, (uint64_t)(kDeg - j))) phi[j >> 6] |= 1ull << (j & 63);
+  J.phish.assign((size_t)64 * (kPW + 1), 0);
+  for (int s2 = 0; s2 < 64; ++s2)
+    for (int q = 0; q <= kPW; ++q) {
+      const uint64_t lo = phi[q] << s2;
+      const uint64_t hi = (q > 0 && s2) ? phi[q - 1] >> (64 - s2) : 0;
+      J.phish[(size_t)s2 * (kPW + 1) + q] = lo | hi;
+    }
+  std::vector<uint64_t> one(kPW, 0), x1(kPW, 0);
+  one[0] = 1;
+  x1[0] = 2;
+  J.polys.push_back(one);
+  J.polys.push_back(powmod(x1, kMtBlockOutputs, J.phish));
+  return true;
+}
+
+// the jump polynomials of substreams 0 .. blocks-1 on `device` (host work once per process)
+const uint64_t* jump_polys(uint64_t blocks, int device, const char** err) {
+  JumpTable& J = jump_table();
+  std::lock_guard<std::mutex> lock(J.mu);
+  if (!J.ready) {
+    if (!build_phi(J)) {
+      *err = J.error.c_str();
+      return nullptr;
+    }
+    J.ready = true;
+  }
+  if (J.polys.size() < blocks) {
+    const uint64_t have = J.polys.size();
+    J.polys.resize(blocks);
+    const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    const uint64_t per = (blocks - have + nt - 1) / nt;
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) {
+      const uint64_t lo = have + t * per, hi = std::min<uint64_t>(blocks, lo + per);
+      if (lo >= hi) break;
+      th.emplace_back([&J, lo, hi] {
+        std::vector<uint64_t> cur = powmod(J.polys[1], lo, J.phish);
+        for (uint64_t b = lo; b < hi; ++b) {
+          J.polys[b] = cur;
+          if (b + 1 < hi) cur = mulmod(cur, J.polys[1], J.phish);
+        }
+      });
+    }
+    for (auto& x : th) x.join();
+  }
+  auto& d = J.dev[device];
+  if (d.second < blocks) {  // the old copy is kept: kernels in flight may still read it
+    uint64_t* p = nullptr;
+    if (cudaMalloc(&p, blocks * kPW * 8) != cudaSuccess) {
+      *err = "cudaMalloc of the jump polynomials failed";
+      return nullptr;
+    }
+    std::vector<uint64_t> flat(blocks * kPW);
+    for (uint64_t b = 0; b < blocks; ++b) std::memcpy(&flat[b * kPW], J.polys[b].data(), kPW * 8);
+    cudaMemcpy(p, flat.data(), flat.size() * 8, cudaMemcpyHostToDevice);
+    d = {p, blocks};
+  }
+  return d.first;
 }
 
 __global__ void first_pass(const uint32_t* __restrict__ draws, uint64_t len, uint64_t ndraws,
@@ -255,16 +530,78 @@ unsigned sm_grid(uint64_t n, int block) {
 
 }  // namespace
 
-void launch_random_indices(uint64_t engine_seed, uint64_t len, uint64_t count,
-                           const RandomScratch& s, cudaStream_t stream) {
-  count_launches(len > count ? 7 : 4);
+// CPU check of the jump-ahead (tests): the window of substream b computed by the correlation
+// with P_b against the engine advanced output by output; 0 when every word agrees (the first
+// word up to its 31 low bits, which the twist never reads) and the next 312 outputs match
+int mt_jump_check(uint64_t engine_seed, uint64_t b, const char** err) {
+  JumpTable& J = jump_table();
+  {
+    std::lock_guard<std::mutex> lock(J.mu);
+    if (!J.ready) {
+      if (!build_phi(J)) {
+        *err = J.error.c_str();
+        return -1;
+      }
+      J.ready = true;
+    }
+    if (b >= 2 && J.polys.size() <= b) {
+      for (uint64_t q = J.polys.size(); q <= b; ++q) J.polys.push_back(mulmod(J.polys[q - 1], J.polys[1], J.phish));
+    }
+  }
+  const uint64_t total = b * kMtBlockOutputs + 2 * kMtN + kMtSeqWords;
+  std::vector<uint64_t> x(total);
+  uint64_t v = engine_seed;
+  x[0] = v;
+  for (int i = 1; i < kMtN; ++i) {
+    v = 6364136223846793005ULL * (v ^ (v >> 62)) + (uint64_t)i;
+    x[i] = v;
+  }
+  for (uint64_t k = kMtN; k < total; ++k) x[k] = twist_word(x[k - kMtN], x[k - kMtN + 1], x[k - kMtN + 156]);
+  std::vector<uint64_t> w(kMtN, 0);
+  const std::vector<uint64_t>& P = J.polys[b];
+  for (int i = 0; i < kDeg; ++i)
+    if ((P[i >> 6] >> (i & 63)) & 1u)
+      for (int j = 0; j < kMtN; ++j) w[j] ^= x[i + j];
+  const uint64_t base = b * kMtBlockOutputs;
+  if ((w[0] ^ x[base]) & 0xFFFFFFFF80000000ULL) return 1;
+  for (int j = 1; j < kMtN; ++j)
+    if (w[j] != x[base + j]) return 2;
+  std::vector<uint64_t> ext(w);  // the next twist from the computed window
+  for (int k = 0; k < kMtN; ++k) ext.push_back(twist_word(ext[k], ext[k + 1], ext[k + 156]));
+  for (int k = 0; k < kMtN; ++k)
+    if (temper(ext[kMtN + k]) != temper(x[base + kMtN + k])) return 3;
+  return 0;
+}
+
+int launch_random_indices(uint64_t engine_seed, uint64_t len, uint64_t count, const RandomScratch& s,
+                          cudaStream_t stream, const char** err) {
   const uint64_t words = (len + 31) / 32;
   cudaMemsetAsync(s.bitmap, 0, words * sizeof(uint32_t), stream);
   if (count >= len) {
+    count_launches(4);
     fill_prefix<<<sm_grid(words, 256), 256, 0, stream>>>(s.bitmap, len);
   } else {
     const uint64_t ndraws = len - count;
-    mt_draws_kernel<<<1, kMtThreads, 0, stream>>>(engine_seed, len, ndraws, s.draws);
+    const uint64_t blocks = (ndraws + kMtBlockOutputs - 1) / kMtBlockOutputs;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t* polys = jump_polys(blocks, dev, err);
+    if (!polys) return DMB_CUDA;
+    count_launches(9);
+    // DMB_MT_FORCE_FIXUP=1 (tests): report a rejection at output 0, so the sequential replay
+    // rewrites every draw -- it must reproduce the substreams' draws exactly
+    const char* ff = std::getenv("DMB_MT_FORCE_FIXUP");
+    cudaMemsetAsync(s.mt_reject, (ff && ff[0] == '1') ? 0x00 : 0xff, sizeof(unsigned long long), stream);
+    mt_seq_kernel<<<1, kMtThreads, 0, stream>>>(engine_seed, s.mt_seq);
+    const int smem = (int)((kMtSeqWords + 2 * kMtN) * 8);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(mt_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    mt_block_kernel<<<(unsigned)blocks, kMtThreads, smem, stream>>>(s.mt_seq, polys, len, ndraws, s.draws,
+                                                                    s.mt_windows, s.mt_reject);
+    mt_fixup_kernel<<<1, kMtThreads, 0, stream>>>(s.mt_windows, len, ndraws, s.draws, s.mt_reject);
     cudaMemsetAsync(s.first, 0xff, len * sizeof(uint32_t), stream);
     cudaMemsetAsync(s.second, 0xff, len * sizeof(uint32_t), stream);
     first_pass<<<sm_grid(ndraws, 256), 256, 0, stream>>>(s.draws, len, ndraws, s.first);
@@ -276,6 +613,7 @@ void launch_random_indices(uint64_t engine_seed, uint64_t len, uint64_t count,
   block_popc<<<(unsigned)blocks, kScanBlock, 0, stream>>>(s.bitmap, words, partial);
   scan_partials<<<1, kScanBlock, 0, stream>>>(partial, blocks);
   word_ranks<<<(unsigned)blocks, kScanBlock, 0, stream>>>(s.bitmap, words, partial, s.rank, s.idx);
+  return DMB_OK;
 }
 
 }  // namespace dmb

@@ -93,3 +93,19 @@ def test_sort16_network():
         hi, lo = np.maximum(x[:, i], x[:, j]), np.minimum(x[:, i], x[:, j])
         x[:, i], x[:, j] = hi, lo
     assert (np.diff(x, axis=1) <= 0).all()
+
+
+@pytest.mark.parametrize("seed,block", [(12345, 1), (12345, 2), (987654321, 3), (2**63 + 5, 7), (1, 11)])
+def test_mt19937_64_jump_ahead_is_exact(seed, block):
+    """The Random scheme's substreams (random_index.cu): the start window of substream b, from
+    the jump polynomial x^(b W) mod phi (phi by Berlekamp-Massey) correlated with the seeded
+    engine's first words, equals the engine advanced b W outputs one by one (the first
+    word up to its 31 low bits, never read by the twist), and the next 312 outputs match."""
+    import ctypes as C
+
+    from paper_2502_06728_b200 import _capi
+
+    f = _capi.lib.dmb_debug_mt_jump_check
+    f.argtypes = [C.c_uint64, C.c_uint64]
+    f.restype = C.c_int
+    assert f(seed, block) == 0

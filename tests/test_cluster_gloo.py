@@ -121,3 +121,43 @@ def test_hybrid_groups_and_reduce_scatter():
     mp.spawn(_groups_worker, args=(4, _free_port(), results), nprocs=4, join=True)
     for r in range(4):
         assert results[r] == (True, True, True), (r, results[r])
+
+
+def _bucket_exchange_worker(rank, world, port, results):
+    """CollectiveExchange (the cluster's bucketed exchange): every bucket's bodies arrive in
+    member order, whatever order the gathers complete in, and the agreement max-reduces the
+    refusal flags over the world."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2502_06728_b200.cluster import CollectiveExchange
+
+    ex = CollectiveExchange(None, dist.group.WORLD, None, members=world, shard_members=1)
+    xfers = [48, 16, 112]
+    ex.setup(xfers, "cpu")
+    ex.begin_step()
+    handles = []
+    for bi, x in enumerate(xfers):
+        ex.own(bi).copy_(torch.arange(x, dtype=torch.int64).to(torch.uint8) ^ (17 * rank + bi))
+        handles.append(ex.start(bi))
+    ok = True
+    for bi in reversed(range(len(xfers))):  # merges may consume buckets in any order
+        ptrs = ex.bodies(bi, handles[bi])
+        base = ex.gathered[bi].data_ptr()
+        for r in range(world):
+            x = xfers[bi]
+            ok &= ptrs[r] == base + r * x
+            want = torch.arange(x, dtype=torch.int64).to(torch.uint8) ^ (17 * r + bi)
+            ok &= bool(torch.equal(ex.gathered[bi][r * x:(r + 1) * x], want))
+    flag = torch.tensor([1 if rank == world - 1 else 0], dtype=torch.int32)
+    ex.agree(flag)
+    results[rank] = (bool(ok), int(flag.item()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_bucketed_exchange_and_agreement(world):
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_bucket_exchange_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    for r in range(world):
+        assert results[r] == (True, 1), (r, results[r])

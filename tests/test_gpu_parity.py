@@ -654,3 +654,17 @@ def test_tc_near_ties_settle_in_fixup(oracle, monkeypatch, sign, dtype):
     chunk_close(host(ead), ew, 64, what="exp_avg")
     chunk_close(host(esd), sw, 64, what="exp_avg_sq")
     update_close(host(pd), pw, p0, lr, 64)
+
+
+@pytest.mark.parametrize("L,c", [(300001, 1 / 16), (200000, 1 / 2)])
+def test_random_substream_replay_matches_oracle(oracle, monkeypatch, L, c):
+    """DMB_MT_FORCE_FIXUP=1 reports a Lemire rejection at output 0, so the exact sequential
+    replay (random_index.cu, mt_fixup_kernel) rewrites every draw from the substream windows:
+    the index set must still be bit-exact (the path a real rejection, p < 2^-32 per draw, takes)."""
+    p = P()
+    monkeypatch.setenv("DMB_MT_FORCE_FIXUP", "1")
+    rep = Rep(scheme=RANDOM, compression=c, seed=4321)
+    for step in (11, 12):
+        want = oracle.selected_indices(rep, step, 1, L)
+        got = p.selected_indices(rep_to_cfg(rep), step, 1, L).cpu().numpy()
+        assert np.array_equal(got, want.astype(np.int64)), step
