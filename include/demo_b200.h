@@ -19,6 +19,10 @@
  *   adamw_prepare         optim.hpp:52      .cpp:51     dmb_adamw_prepare
  *   adamw_apply           optim.hpp:59      .cpp:57     dmb_adamw_apply
  *   baseline_sgd_step     optim.hpp:66      .cpp:76     dmb_baseline_sgd_step
+ *   chunk_layout / chunk / unchunk  transform.hpp:20-26  dmb_chunk_layout / dmb_chunk / dmb_unchunk
+ *   dct2 / idct3 (DctPlan) transform.hpp:28-53         dmb_dct2 / dmb_idct3
+ *   extract_fast_components transform.hpp:55-71        dmb_extract_fast_components
+ *   sign_transform        transform.hpp:73              dmb_sign_transform
  *   grad_reduce_scatter   cluster.hpp:78    .cpp:63     dmb_grad_mean (local mean; the
  *                                                       split/exchange is NCCL's)
  *   run_step_hybrid schedule (per shard: decode_and_merge + apply, cluster.cpp:193-231)
@@ -126,6 +130,31 @@ int dmb_plan_update(const dmb_rep_cfg* cfg, uint64_t len, uint64_t step, uint32_
                     dmb_update* out);
 /* device bytes a body needs for this cfg/len at any step (16-byte rounded) */
 uint64_t dmb_update_capacity(const dmb_rep_cfg* cfg, uint64_t len);
+
+/* ---- transform.hpp:13-74 (device FP32 vectors; the DCTs accumulate in FP64 in the
+ * reference's order from its libm basis, size <= 1024) --------------------------- */
+/* ChunkLayout, transform.hpp:13-18 */
+typedef struct {
+  uint64_t length;
+  uint64_t chunk_size;
+  uint64_t num_chunks;
+  uint64_t pad; /* zeros appended to the last chunk */
+} dmb_layout;
+/* chunk_layout, transform.hpp:20 / .cpp:17-25 (host only) */
+int dmb_chunk_layout(uint64_t length, uint64_t chunk_size, dmb_layout* out);
+/* chunk / unchunk, transform.hpp:23-26 / .cpp:27-39: rows = num_chunks x chunk_size, pad zeroed */
+int dmb_chunk(dmb_ctx* ctx, const float* v, const dmb_layout* layout, float* rows, void* stream);
+int dmb_unchunk(dmb_ctx* ctx, const float* rows, const dmb_layout* layout, float* v, void* stream);
+/* dct2 / idct3 (DctPlan::forward / inverse), transform.hpp:28-53: `count` vectors of `size` */
+int dmb_dct2(dmb_ctx* ctx, const float* x, uint64_t size, uint64_t count, float* out, void* stream);
+int dmb_idct3(dmb_ctx* ctx, const float* coeffs, uint64_t size, uint64_t count, float* out, void* stream);
+/* extract_fast_components, transform.hpp:55-71 / .cpp:94-155: indices (num_chunks * top_k,
+ * chunk local, ascending), coeffs, fast and residual = v - fast (each output nullable but fast) */
+int dmb_extract_fast_components(dmb_ctx* ctx, const float* v, uint64_t len, uint64_t chunk_size,
+                                uint64_t top_k, uint32_t* indices, float* coeffs, float* fast,
+                                float* residual, void* stream);
+/* sign_transform, transform.hpp:73 / .cpp:157-161 (in place) */
+int dmb_sign_transform(dmb_ctx* ctx, float* v, uint64_t n, void* stream);
 
 /* ---- replicate.hpp ---------------------------------------------------------- */
 int dmb_selected_indices(dmb_ctx* ctx, const dmb_rep_cfg* cfg, uint64_t step, uint32_t shard,

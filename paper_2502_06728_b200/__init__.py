@@ -11,4 +11,6 @@ from .core import (CompressedUpdate, ConfigError, CudaError, DemoError, EncodeRe
                    baseline_sgd_step, decode_and_merge, demo_sgd_apply, demo_sgd_prepare, deserialize,
                    fallback_chunks, grad_mean, launch_count, merge_apply_adamw, merge_apply_sgd, plan_update,
                    select_and_encode, selected_indices, serialize, status, value_bits, wire_bytes)
+from .core import (ChunkLayout, Extraction, FreqSelection, chunk, chunk_layout, dct2,  # noqa: F401
+                   extract_fast_components, idct3, sign_transform, unchunk)
 from ._capi import LIB_PATH  # noqa: F401

@@ -9,7 +9,9 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdemo_b200.so")
+# DMB_LIB selects another build of the same library (tools/kernel_timeline.py loads the one
+# compiled with -DDMB_KERNEL_EVENTS); it is never a CPU substitute
+LIB_PATH = os.environ.get("DMB_LIB") or os.path.join(HERE, "libdemo_b200.so")
 
 DMB_OK, DMB_TRAINING, DMB_CONFIG, DMB_PROTOCOL, DMB_CUDA = 0, 1, 2, 3, 4
 ABI_VERSION = 1
@@ -99,6 +101,13 @@ _SIGS = {
     "dmb_launch_count": (U64, [P]),
     "dmb_set_wire_format": (C.c_int, [P, C.c_int32]),
     "dmb_plan_exchange": (C.c_int, [P, PCFG, U64, U64, U32, PUPD]),
+    "dmb_chunk_layout": (C.c_int, [U64, U64, P]),
+    "dmb_chunk": (C.c_int, [P, P, P, P, P]),
+    "dmb_unchunk": (C.c_int, [P, P, P, P, P]),
+    "dmb_dct2": (C.c_int, [P, P, U64, U64, P, P]),
+    "dmb_idct3": (C.c_int, [P, P, U64, U64, P, P]),
+    "dmb_extract_fast_components": (C.c_int, [P, P, U64, U64, U64, P, P, P, P, P]),
+    "dmb_sign_transform": (C.c_int, [P, P, U64, P]),
     "dmb_latch_export": (C.c_int, [P, P, P]),
     "dmb_latch_import": (C.c_int, [P, P, P]),
     "dmb_kernel_timer_enable": (C.c_int, [C.c_int]),

@@ -459,3 +459,107 @@ def grad_mean(grads: Sequence[torch.Tensor]) -> torch.Tensor:
     arr = (C.c_void_p * len(grads))(*[g.data_ptr() for g in grads])
     _check(lib.dmb_grad_mean(context(out.device).h, arr, len(grads), out.numel(), _ptr(out), _stream(out)))
     return out
+
+
+# ---------------------------------------------------------------- transform.hpp:13-74
+@dataclass
+class ChunkLayout:
+    """transform.hpp:13-18"""
+    length: int = 0
+    chunk_size: int = 0
+    num_chunks: int = 0
+    pad: int = 0
+
+
+class _Layout(C.Structure):
+    _fields_ = [("length", C.c_uint64), ("chunk_size", C.c_uint64), ("num_chunks", C.c_uint64),
+                ("pad", C.c_uint64)]
+
+
+def chunk_layout(length: int, chunk_size: int) -> ChunkLayout:
+    """transform.hpp:20 (ConfigError on chunk_size 0, transform.cpp:18)"""
+    out = _Layout()
+    _check(lib.dmb_chunk_layout(length, chunk_size, C.byref(out)))
+    return ChunkLayout(out.length, out.chunk_size, out.num_chunks, out.pad)
+
+
+def _layout_c(layout: ChunkLayout) -> _Layout:
+    return _Layout(layout.length, layout.chunk_size, layout.num_chunks, layout.pad)
+
+
+def chunk(v: torch.Tensor, layout: ChunkLayout) -> torch.Tensor:
+    """transform.hpp:22-23: num_chunks x chunk_size rows, pad tail zeroed (flat)"""
+    _vec(v, "v")
+    if v.numel() != layout.length:
+        raise ConfigError("chunk: layout does not match the vector")
+    rows = torch.empty(layout.num_chunks * layout.chunk_size, dtype=torch.float32, device=v.device)
+    lc = _layout_c(layout)
+    _check(lib.dmb_chunk(context(v.device).h, _ptr(v), C.byref(lc), _ptr(rows), _stream(v)))
+    return rows
+
+
+def unchunk(rows: torch.Tensor, layout: ChunkLayout) -> torch.Tensor:
+    """transform.hpp:25-26: concatenated rows without the pad tail"""
+    _vec(rows, "rows")
+    if rows.numel() != layout.num_chunks * layout.chunk_size:
+        raise ConfigError("unchunk: row buffer does not match the layout")
+    v = torch.empty(layout.length, dtype=torch.float32, device=rows.device)
+    lc = _layout_c(layout)
+    _check(lib.dmb_unchunk(context(rows.device).h, _ptr(rows), C.byref(lc), _ptr(v), _stream(rows)))
+    return v
+
+
+def _dct(x: torch.Tensor, inverse: bool) -> torch.Tensor:
+    _vec(x, "x")
+    size = x.shape[-1] if x.dim() > 1 else x.numel()
+    count = x.numel() // size if size else 0
+    out = torch.empty_like(x)
+    f = lib.dmb_idct3 if inverse else lib.dmb_dct2
+    _check(f(context(x.device).h, _ptr(x), size, count, _ptr(out), _stream(x)))
+    return out
+
+
+def dct2(x: torch.Tensor) -> torch.Tensor:
+    """transform.hpp:51 (DctPlan::forward); a 2-D tensor transforms each row"""
+    return _dct(x, False)
+
+
+def idct3(coeffs: torch.Tensor) -> torch.Tensor:
+    """transform.hpp:52 (DctPlan::inverse); a 2-D tensor transforms each row"""
+    return _dct(coeffs, True)
+
+
+@dataclass
+class FreqSelection:
+    """transform.hpp:55-62"""
+    layout: ChunkLayout
+    top_k: int
+    indices: torch.Tensor  # int32 (uint32 values), num_chunks * top_k, chunk local, ascending
+    coeffs: torch.Tensor
+
+
+@dataclass
+class Extraction:
+    """transform.hpp:64-68"""
+    selection: FreqSelection
+    fast: torch.Tensor
+    residual: torch.Tensor
+
+
+def extract_fast_components(v: torch.Tensor, chunk_size: int, top_k: int) -> Extraction:
+    """transform.hpp:70-71 / transform.cpp:94-155"""
+    _vec(v, "v")
+    layout = chunk_layout(v.numel(), chunk_size)
+    n = layout.num_chunks * top_k if 1 <= top_k <= chunk_size else 0
+    idx = torch.empty(max(n, 1), dtype=torch.int32, device=v.device)
+    co = torch.empty(max(n, 1), dtype=torch.float32, device=v.device)
+    fast, res = torch.empty_like(v), torch.empty_like(v)
+    _check(lib.dmb_extract_fast_components(context(v.device).h, _ptr(v), v.numel(), chunk_size, top_k, _ptr(idx),
+                                           _ptr(co), _ptr(fast), _ptr(res), _stream(v)))
+    return Extraction(FreqSelection(layout, top_k, idx[:n], co[:n]), fast, res)
+
+
+def sign_transform(v: torch.Tensor) -> None:
+    """transform.hpp:73 (in place)"""
+    _vec(v, "v")
+    _check(lib.dmb_sign_transform(context(v.device).h, _ptr(v), v.numel(), _stream(v)))

@@ -147,6 +147,8 @@ struct dmb_ctx {
   unsigned* fb_count = nullptr;
   uint64_t fb_cap = 0;
   int wire_format = DMB_WIRE_REFERENCE;  // DeMo exchange layout of the updates encoded here
+  uint8_t* scratch = nullptr;             // extract_fast_components' payload body
+  uint64_t scratch_cap = 0;
 };
 
 namespace {
@@ -387,7 +389,7 @@ int ensure_random(dmb_ctx* ctx, const dmb_rep_cfg* cfg, uint64_t step, uint32_t 
     ctx->rnd_len_cap = len;
   }
   RandomScratch& r = ctx->rnd;
-  const uint64_t blocks = (len + kMtBlockOutputs - 1) / kMtBlockOutputs;
+  const uint64_t blocks = kMtMaxSubstreams;
   if (!r.mt_seq) {
     DMB_CUDA_TRY(cudaMalloc(&r.mt_seq, kMtSeqWords * 8));
     DMB_CUDA_TRY(cudaMalloc(&r.mt_reject, sizeof(unsigned long long)));
@@ -624,6 +626,7 @@ int dmb_ctx_destroy(dmb_ctx* ctx) {
   cudaFree(r.mt_seq);
   cudaFree(r.mt_windows);
   cudaFree(r.mt_reject);
+  cudaFree(ctx->scratch);
   cudaFree(ctx->status);
   cudaFree(ctx->aux);
   delete ctx;
@@ -1060,6 +1063,93 @@ int dmb_fallback_chunks(dmb_ctx* ctx, void* stream, uint64_t* count) {
   DMB_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
   *count = a.fallback_chunks + b.fallback_chunks;
   return DMB_OK;
+}
+
+// ---- transform.hpp:13-74 -------------------------------------------------------
+int dmb_chunk_layout(uint64_t length, uint64_t chunk_size, dmb_layout* out) {
+  if (!out) return fail(DMB_CONFIG, "NULL argument");
+  if (chunk_size == 0) return fail(DMB_CONFIG, "chunk size must be positive");  // transform.cpp:18
+  out->length = length;
+  out->chunk_size = chunk_size;
+  out->num_chunks = (length + chunk_size - 1) / chunk_size;
+  out->pad = out->num_chunks * chunk_size - length;
+  return DMB_OK;
+}
+
+int dmb_chunk(dmb_ctx* ctx, const float* v, const dmb_layout* layout, float* rows, void* stream) {
+  (void)ctx;
+  if (!layout || layout->chunk_size == 0) return fail(DMB_CONFIG, "chunk: layout does not match the vector");
+  const uint64_t padded = layout->num_chunks * layout->chunk_size;
+  if (padded) launch_chunk(v, layout->length, padded, rows, as_stream(stream));
+  return last_launch();
+}
+
+int dmb_unchunk(dmb_ctx* ctx, const float* rows, const dmb_layout* layout, float* v, void* stream) {
+  (void)ctx;
+  if (!layout || layout->chunk_size == 0) return fail(DMB_CONFIG, "unchunk: row buffer does not match the layout");
+  if (layout->length) launch_copy(rows, layout->length, v, as_stream(stream));
+  return last_launch();
+}
+
+static int dct_common(dmb_ctx* ctx, bool inverse, const float* in, uint64_t size, uint64_t count, float* out,
+                      void* stream) {
+  if (size == 0) return fail(DMB_CONFIG, "transform size must be positive");  // transform.cpp:43
+  if (size > 1024) return fail(DMB_CONFIG, "transform size %llu above the device limit 1024", (unsigned long long)size);
+  if (!count) return DMB_OK;
+  Basis b{};
+  if (int rc = get_basis(ctx, (int)size, &b)) return rc;
+  launch_dct(inverse, in, size, count, b, out, as_stream(stream));
+  return last_launch();
+}
+
+int dmb_dct2(dmb_ctx* ctx, const float* x, uint64_t size, uint64_t count, float* out, void* stream) {
+  return dct_common(ctx, false, x, size, count, out, stream);
+}
+
+int dmb_idct3(dmb_ctx* ctx, const float* coeffs, uint64_t size, uint64_t count, float* out, void* stream) {
+  return dct_common(ctx, true, coeffs, size, count, out, stream);
+}
+
+int dmb_sign_transform(dmb_ctx* ctx, float* v, uint64_t n, void* stream) {
+  (void)ctx;
+  if (n) launch_sign(v, n, as_stream(stream));
+  return last_launch();
+}
+
+int dmb_extract_fast_components(dmb_ctx* ctx, const float* v, uint64_t len, uint64_t chunk_size, uint64_t top_k,
+                                uint32_t* indices, float* coeffs, float* fast, float* residual, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (top_k == 0 || top_k > chunk_size)  // transform.cpp:96-101
+    return fail(DMB_CONFIG, "top_k %llu out of range for chunk size %llu", (unsigned long long)top_k,
+                (unsigned long long)chunk_size);
+  dmb_rep_cfg cfg{};
+  cfg.scheme = DMB_DEMO;
+  cfg.sign_mode = 0;
+  cfg.transfer_dtype = DMB_FP32;  // fp32 values are the coefficients, not narrowed (replicate.cpp:137-144)
+  cfg.chunk_size = chunk_size;
+  cfg.top_k = top_k;
+  cfg.compression = (double)top_k / (double)chunk_size;
+  const uint64_t cap = capacity(&cfg, len);
+  if (cap > ctx->scratch_cap) {
+    cudaFree(ctx->scratch);
+    DMB_CUDA_TRY(cudaMalloc(&ctx->scratch, cap));
+    ctx->scratch_cap = cap;
+  }
+  dmb_update u{};
+  u.body = ctx->scratch;
+  const int wf = ctx->wire_format;
+  ctx->wire_format = DMB_WIRE_REFERENCE;
+  if (int rc = clear_aux(ctx, s)) return rc;
+  const int rc = encode(ctx, ctx->aux, false, v, nullptr, nullptr, 0.0, len, &cfg, 0, 0, &u, fast, nullptr, s);
+  ctx->wire_format = wf;
+  if (rc) return rc;
+  const uint64_t n = u.n_values;  // num_chunks * top_k
+  if (n) {
+    if (indices) DMB_CUDA_TRY(cudaMemcpyAsync(indices, ctx->scratch, n * 4, cudaMemcpyDeviceToDevice, s));
+    if (coeffs) DMB_CUDA_TRY(cudaMemcpyAsync(coeffs, ctx->scratch + n * 4, n * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  if (residual && len) launch_residual(v, fast, len, top_k == chunk_size, residual, s);
+  return last_launch();
 }
 
 // test hook (not in the public header): the MT19937-64 jump-ahead of substream b, on the host

@@ -681,6 +681,7 @@ __global__ void __maxnreg__(128)
     const uint32_t tl = (uint32_t)(32 * (warp & 3)) << 16;
     const AdamScalars A = a.adam;
     auto front = [&](uint64_t t, uint32_t n) {
+      evt(a, tid == 32 * kSelWarps, n, 2);
       mbar_wait(bar_g, n & 1);
       float l1 = 0.f;
       bool fin = true;
@@ -738,6 +739,7 @@ __global__ void __maxnreg__(128)
         mbar_arrive(bar_x);
         mbar_arrive(&bar_l[n & 1]);
       }
+      evt(a, tid == 32 * kSelWarps, n, 3);
     };
     if (kFwd && tile < ntiles) front(tile, 0);
     if (kFwd && tile + G < ntiles) {

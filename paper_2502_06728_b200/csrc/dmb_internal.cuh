@@ -223,6 +223,14 @@ void launch_striding_iota(uint32_t* out, uint64_t offset, uint64_t period, uint6
 void launch_unpack_values(const uint8_t* vals, uint64_t n, int dtype, float* out,
                           cudaStream_t stream);
 
+// transform.hpp surface (transform.cu)
+void launch_chunk(const float* v, uint64_t len, uint64_t padded, float* rows, cudaStream_t st);
+void launch_copy(const float* a, uint64_t n, float* out, cudaStream_t st);
+void launch_dct(bool inverse, const float* in, uint64_t n, uint64_t count, const Basis& b, float* out,
+                cudaStream_t st);
+void launch_sign(float* v, uint64_t n, cudaStream_t st);
+void launch_residual(const float* v, const float* fast, uint64_t n, bool full_band, float* res, cudaStream_t st);
+
 // Random index sets (replicate.cpp:160-172) on the device.
 struct RandomScratch {
   uint32_t* draws;   // j_i for the L - count iterations that decide the set
@@ -233,13 +241,13 @@ struct RandomScratch {
   uint32_t* idx;     // sorted selected indices
   uint64_t capacity; // elements
   // MT19937-64 substreams (random_index.cu): the engine's first words, the start window of
-  // every block of kMtBlockOutputs outputs, the first output a Lemire rejection may touch
+  // every substream, the first output a Lemire rejection may touch
   uint64_t* mt_seq;
   uint64_t* mt_windows;
   uint64_t mt_blocks_cap;
   unsigned long long* mt_reject;
 };
-constexpr uint64_t kMtBlockOutputs = 312ull * 128ull;  // engine outputs per substream
+constexpr uint64_t kMtMaxSubstreams = 4096;           // substream windows held per context
 constexpr uint64_t kMtSeqWords = 312ull * 65ull;       // seeded words + 64 twists (>= 19937 + 312)
 // returns DMB_OK or DMB_CUDA (message in *err)
 int launch_random_indices(uint64_t engine_seed, uint64_t len, uint64_t count, const RandomScratch& s,

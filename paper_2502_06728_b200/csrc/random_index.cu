@@ -8,7 +8,7 @@
 // Only the iterations i = L .. count+1 decide WHICH values end in positions
 // [0, count); the later ones permute that prefix among itself and the result is
 // sorted anyway.  So (1) the draws j_i of those L - count iterations come from the
-// MT19937-64 stream split into substreams of kMtBlockOutputs outputs, one CTA each, every
+// MT19937-64 stream split into one wave of substreams (two per CTA), every
 // substream started by a GF(2) jump-ahead (below); Lemire's debias rejects an output with
 // probability < 2^-32, and a rejection shifts every later draw by one output, so the CTAs
 // assume none and report the first output that could be one -- an exact sequential
@@ -46,7 +46,6 @@ namespace {
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr int kMtN = 312;
 constexpr int kMtThreads = 320;
-constexpr uint64_t kMtTwists = kMtBlockOutputs / kMtN;  // twists per substream
 
 __host__ __device__ __forceinline__ uint64_t temper(uint64_t y) {
   y ^= (y >> 29) & 0x5555555555555555ULL;
@@ -104,47 +103,64 @@ __device__ __forceinline__ uint32_t lemire(uint64_t x, uint64_t n, bool& rejecte
   return (uint32_t)__umul64hi(x, n);
 }
 
-// Substream b: window P_b(T) s0 by correlation, then kMtTwists twists; draw d = output o
-// (no rejection before o assumed; the first possible rejection is reported in *reject)
-__global__ void __launch_bounds__(kMtThreads) mt_block_kernel(const uint64_t* __restrict__ seq,
-                                                              const uint64_t* __restrict__ polys, uint64_t len,
-                                                              uint64_t ndraws, uint32_t* __restrict__ draws,
-                                                              uint64_t* __restrict__ windows,
-                                                              unsigned long long* __restrict__ reject) {
+// Substreams: W outputs each (a multiple of 312), kSubPerCta per CTA (their twists share the
+// CTA's barriers).  Substream b: window P_b(T) s0 by correlation, then W / 312 twists on
+// ping-pong windows (two barriers per twist); draw d = output o (no rejection before o
+// assumed; the first output that could be one is reported in *reject)
+constexpr int kSubPerCta = 2;
+constexpr int kBlockThreads = kSubPerCta * kMtThreads;
+
+__global__ void __launch_bounds__(kBlockThreads) mt_block_kernel(const uint64_t* __restrict__ seq,
+                                                                 const uint64_t* __restrict__ polys, uint64_t W,
+                                                                 uint64_t nsub, uint64_t len, uint64_t ndraws,
+                                                                 uint32_t* __restrict__ draws,
+                                                                 uint64_t* __restrict__ windows,
+                                                                 unsigned long long* __restrict__ reject) {
   extern __shared__ uint64_t sm[];
-  uint64_t* xs = sm;                   // the engine's first kMtSeqWords words
-  uint64_t* poly = xs + kMtSeqWords;   // P_b, bit i = coefficient of x^i
-  uint64_t* mt = poly + kMtN;          // the substream's window
-  const int t = threadIdx.x;
-  const uint64_t b = blockIdx.x;
-  if (b == 0) {
-    if (t < kMtN) mt[t] = seq[t];
-  } else {
-    for (uint64_t i = t; i < kMtSeqWords; i += kMtThreads) xs[i] = seq[i];
-    if (t < kMtN) poly[t] = polys[b * kMtN + t];
-    __syncthreads();
-    if (t < kMtN) {
-      uint64_t acc = 0;
-      for (int w = 0; w < kMtN; ++w) {  // uniform across the CTA: no divergence
-        uint64_t bits = poly[w];
+  uint64_t* xs = sm;                               // the engine's first kMtSeqWords words
+  uint64_t* poly = xs + kMtSeqWords;               // [sub][312]: P_b, bit i = coefficient of x^i
+  uint64_t* win = poly + kSubPerCta * kMtN;        // [sub][2][312]: ping-pong windows
+  const int sub = threadIdx.x / kMtThreads, t = threadIdx.x % kMtThreads;
+  const uint64_t b = (uint64_t)blockIdx.x * kSubPerCta + sub;
+  const bool live = b < nsub && t < kMtN;
+  for (uint64_t i = threadIdx.x; i < kMtSeqWords; i += kBlockThreads) xs[i] = seq[i];
+  if (live) poly[sub * kMtN + t] = b ? polys[b * kMtN + t] : 0ull;
+  __syncthreads();
+  uint64_t* w0 = win + sub * 2 * kMtN;
+  if (live) {
+    uint64_t acc = 0;
+    if (b == 0) {
+      acc = xs[t];
+    } else {
+      const uint32_t* p32 = reinterpret_cast<const uint32_t*>(poly + sub * kMtN);
+      const uint64_t* xt = xs + t;
+      for (int w = 0; w < 2 * kMtN; ++w, xt += 32) {  // uniform within a substream
+        uint32_t bits = p32[w];
         while (bits) {
-          const int i = 64 * w + __ffsll((long long)bits) - 1;
+          const int i = __ffs(bits) - 1;
           bits &= bits - 1;
-          acc ^= xs[i + t];
+          acc ^= xt[i];
         }
       }
-      mt[t] = acc;
     }
+    w0[t] = acc;
+    windows[b * kMtN + t] = acc;
   }
-  __syncthreads();
-  if (t < kMtN) windows[b * kMtN + t] = mt[t];
-  const uint64_t o0 = b * kMtBlockOutputs;
-  for (uint64_t tw = 0; tw < kMtTwists && o0 + tw * kMtN < ndraws; ++tw) {
-    twist_block(mt, t);
+  const uint64_t twists = W / kMtN;
+  const uint64_t o0 = b * W;
+  for (uint64_t tw = 0; tw < twists; ++tw) {
+    const uint64_t* cur = w0 + (tw & 1) * kMtN;
+    uint64_t* nxt = w0 + ((tw + 1) & 1) * kMtN;
+    __syncthreads();  // cur complete (previous twist or the correlation)
+    if (t < 156) nxt[t] = twist_word(cur[t], cur[t + 1], cur[t + 156]);
+    __syncthreads();
+    if (t >= 156 && t < 311) nxt[t] = twist_word(cur[t], cur[t + 1], nxt[t - 156]);
+    if (t == 311) nxt[311] = twist_word(cur[311], nxt[0], nxt[155]);
+    __syncthreads();
     const uint64_t o = o0 + tw * kMtN + t;
-    if (t < kMtN && o < ndraws) {
+    if (live && o < ndraws) {
       bool rej;
-      draws[o] = lemire(temper(mt[t]), len - o, rej);
+      draws[o] = lemire(temper(nxt[t]), len - o, rej);
       if (rej) atomicMin(reject, (unsigned long long)o);
     }
   }
@@ -152,17 +168,18 @@ __global__ void __launch_bounds__(kMtThreads) mt_block_kernel(const uint64_t* __
 
 // The rare case: an output from *reject on was rejected, so every later draw moves by one
 // output.  Replay from the start of that substream, sequentially from the rejection on.
-__global__ void __launch_bounds__(kMtThreads) mt_fixup_kernel(const uint64_t* __restrict__ windows, uint64_t len,
-                                                              uint64_t ndraws, uint32_t* __restrict__ draws,
+__global__ void __launch_bounds__(kMtThreads) mt_fixup_kernel(const uint64_t* __restrict__ windows, uint64_t W,
+                                                              uint64_t len, uint64_t ndraws,
+                                                              uint32_t* __restrict__ draws,
                                                               const unsigned long long* __restrict__ reject) {
   __shared__ uint64_t mt[kMtN];
   __shared__ uint64_t d_shared;
   const uint64_t ostar = *reject;
   if (ostar >= ndraws) return;
   const int t = threadIdx.x;
-  const uint64_t b = ostar / kMtBlockOutputs;
+  const uint64_t b = ostar / W;
   if (t < kMtN) mt[t] = windows[b * kMtN + t];
-  uint64_t o = b * kMtBlockOutputs, d = o;  // no rejection before ostar: draw = output there
+  uint64_t o = b * W, d = o;  // no rejection before ostar: draw = output there
   if (t == 0) d_shared = d;
   __syncthreads();
   while (d < ndraws) {
@@ -190,12 +207,15 @@ __global__ void __launch_bounds__(kMtThreads) mt_fixup_kernel(const uint64_t* __
 constexpr int kDeg = 19937;
 constexpr int kPW = kMtN;  // words of a reduced polynomial (degree < 19937)
 
+struct JumpSet {
+  std::vector<std::vector<uint64_t>> polys;           // x^(b W) mod phi, b = 0, 1, ...
+  std::map<int, std::pair<uint64_t*, uint64_t>> dev;  // device copies (pointer, polys held)
+};
 struct JumpTable {
   std::mutex mu;
   bool ready = false;
-  std::vector<uint64_t> phish;                 // 64 x (kPW + 1) words: phi << s, s = 0..63
-  std::vector<std::vector<uint64_t>> polys;    // x^(b W) mod phi, b = 0, 1, ...
-  std::map<int, std::pair<uint64_t*, uint64_t>> dev;  // device copies (pointer, polys held)
+  std::vector<uint64_t> phish;   // 64 x (kPW + 1) words: phi << s, s = 0..63
+  std::map<uint64_t, JumpSet> sets;  // by substream length W
   std::string error;
 };
 JumpTable& jump_table() {
@@ -340,16 +360,21 @@ bool build_phi(JumpTable& J) {
       const uint64_t hi = (q > 0 && s2) ? phi[q - 1] >> (64 - s2) : 0;
       J.phish[(size_t)s2 * (kPW + 1) + q] = lo | hi;
     }
-  std::vector<uint64_t> one(kPW, 0), x1(kPW, 0);
-  one[0] = 1;
-  x1[0] = 2;
-  J.polys.push_back(one);
-  J.polys.push_back(powmod(x1, kMtBlockOutputs, J.phish));
   return true;
 }
 
-// the jump polynomials of substreams 0 .. blocks-1 on `device` (host work once per process)
-const uint64_t* jump_polys(uint64_t blocks, int device, const char** err) {
+// P_0 = 1 and P_1 = x^W mod phi of a substream length W
+void start_set(JumpTable& J, uint64_t W, JumpSet& S) {
+  std::vector<uint64_t> one(kPW, 0), x1(kPW, 0);
+  one[0] = 1;
+  x1[0] = 2;
+  S.polys.push_back(one);
+  S.polys.push_back(powmod(x1, W, J.phish));
+}
+
+// the jump polynomials of substreams 0 .. blocks-1 of length W on `device` (host work once per
+// process and W)
+const uint64_t* jump_polys(uint64_t W, uint64_t blocks, int device, const char** err) {
   JumpTable& J = jump_table();
   std::lock_guard<std::mutex> lock(J.mu);
   if (!J.ready) {
@@ -359,26 +384,28 @@ const uint64_t* jump_polys(uint64_t blocks, int device, const char** err) {
     }
     J.ready = true;
   }
-  if (J.polys.size() < blocks) {
-    const uint64_t have = J.polys.size();
-    J.polys.resize(blocks);
+  JumpSet& S = J.sets[W];
+  if (S.polys.empty()) start_set(J, W, S);
+  if (S.polys.size() < blocks) {
+    const uint64_t have = S.polys.size();
+    S.polys.resize(blocks);
     const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
     const uint64_t per = (blocks - have + nt - 1) / nt;
     std::vector<std::thread> th;
     for (unsigned t = 0; t < nt; ++t) {
       const uint64_t lo = have + t * per, hi = std::min<uint64_t>(blocks, lo + per);
       if (lo >= hi) break;
-      th.emplace_back([&J, lo, hi] {
-        std::vector<uint64_t> cur = powmod(J.polys[1], lo, J.phish);
+      th.emplace_back([&J, &S, lo, hi] {
+        std::vector<uint64_t> cur = powmod(S.polys[1], lo, J.phish);
         for (uint64_t b = lo; b < hi; ++b) {
-          J.polys[b] = cur;
-          if (b + 1 < hi) cur = mulmod(cur, J.polys[1], J.phish);
+          S.polys[b] = cur;
+          if (b + 1 < hi) cur = mulmod(cur, S.polys[1], J.phish);
         }
       });
     }
     for (auto& x : th) x.join();
   }
-  auto& d = J.dev[device];
+  auto& d = S.dev[device];
   if (d.second < blocks) {  // the old copy is kept: kernels in flight may still read it
     uint64_t* p = nullptr;
     if (cudaMalloc(&p, blocks * kPW * 8) != cudaSuccess) {
@@ -386,7 +413,7 @@ const uint64_t* jump_polys(uint64_t blocks, int device, const char** err) {
       return nullptr;
     }
     std::vector<uint64_t> flat(blocks * kPW);
-    for (uint64_t b = 0; b < blocks; ++b) std::memcpy(&flat[b * kPW], J.polys[b].data(), kPW * 8);
+    for (uint64_t b = 0; b < blocks; ++b) std::memcpy(&flat[b * kPW], S.polys[b].data(), kPW * 8);
     cudaMemcpy(p, flat.data(), flat.size() * 8, cudaMemcpyHostToDevice);
     d = {p, blocks};
   }
@@ -534,7 +561,9 @@ unsigned sm_grid(uint64_t n, int block) {
 // with P_b against the engine advanced output by output; 0 when every word agrees (the first
 // word up to its 31 low bits, which the twist never reads) and the next 312 outputs match
 int mt_jump_check(uint64_t engine_seed, uint64_t b, const char** err) {
+  constexpr uint64_t W = 312ull * 128ull;
   JumpTable& J = jump_table();
+  std::vector<uint64_t> P;
   {
     std::lock_guard<std::mutex> lock(J.mu);
     if (!J.ready) {
@@ -544,11 +573,12 @@ int mt_jump_check(uint64_t engine_seed, uint64_t b, const char** err) {
       }
       J.ready = true;
     }
-    if (b >= 2 && J.polys.size() <= b) {
-      for (uint64_t q = J.polys.size(); q <= b; ++q) J.polys.push_back(mulmod(J.polys[q - 1], J.polys[1], J.phish));
-    }
+    JumpSet& S = J.sets[W];
+    if (S.polys.empty()) start_set(J, W, S);
+    for (uint64_t q = S.polys.size(); q <= b; ++q) S.polys.push_back(mulmod(S.polys[q - 1], S.polys[1], J.phish));
+    P = S.polys[b];
   }
-  const uint64_t total = b * kMtBlockOutputs + 2 * kMtN + kMtSeqWords;
+  const uint64_t total = b * W + 2 * kMtN + kMtSeqWords;
   std::vector<uint64_t> x(total);
   uint64_t v = engine_seed;
   x[0] = v;
@@ -558,11 +588,10 @@ int mt_jump_check(uint64_t engine_seed, uint64_t b, const char** err) {
   }
   for (uint64_t k = kMtN; k < total; ++k) x[k] = twist_word(x[k - kMtN], x[k - kMtN + 1], x[k - kMtN + 156]);
   std::vector<uint64_t> w(kMtN, 0);
-  const std::vector<uint64_t>& P = J.polys[b];
   for (int i = 0; i < kDeg; ++i)
     if ((P[i >> 6] >> (i & 63)) & 1u)
       for (int j = 0; j < kMtN; ++j) w[j] ^= x[i + j];
-  const uint64_t base = b * kMtBlockOutputs;
+  const uint64_t base = b * W;
   if ((w[0] ^ x[base]) & 0xFFFFFFFF80000000ULL) return 1;
   for (int j = 1; j < kMtN; ++j)
     if (w[j] != x[base + j]) return 2;
@@ -582,10 +611,18 @@ int launch_random_indices(uint64_t engine_seed, uint64_t len, uint64_t count, co
     fill_prefix<<<sm_grid(words, 256), 256, 0, stream>>>(s.bitmap, len);
   } else {
     const uint64_t ndraws = len - count;
-    const uint64_t blocks = (ndraws + kMtBlockOutputs - 1) / kMtBlockOutputs;
-    int dev = 0;
+    int dev = 0, sms = 148;
     cudaGetDevice(&dev);
-    const uint64_t* polys = jump_polys(blocks, dev, err);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // substreams: one wave of CTAs, kSubPerCta each, W outputs per substream (a multiple of 312)
+    const uint64_t want = (uint64_t)sms * kSubPerCta;
+    const uint64_t W = ((ndraws + want * kMtN - 1) / (want * kMtN)) * kMtN;
+    const uint64_t nsub = (ndraws + W - 1) / W;
+    if (nsub > s.mt_blocks_cap) {
+      *err = "substream windows scratch too small";
+      return DMB_CUDA;
+    }
+    const uint64_t* polys = jump_polys(W, nsub, dev, err);
     if (!polys) return DMB_CUDA;
     count_launches(9);
     // DMB_MT_FORCE_FIXUP=1 (tests): report a rejection at output 0, so the sequential replay
@@ -593,15 +630,16 @@ int launch_random_indices(uint64_t engine_seed, uint64_t len, uint64_t count, co
     const char* ff = std::getenv("DMB_MT_FORCE_FIXUP");
     cudaMemsetAsync(s.mt_reject, (ff && ff[0] == '1') ? 0x00 : 0xff, sizeof(unsigned long long), stream);
     mt_seq_kernel<<<1, kMtThreads, 0, stream>>>(engine_seed, s.mt_seq);
-    const int smem = (int)((kMtSeqWords + 2 * kMtN) * 8);
+    const int smem = (int)((kMtSeqWords + 3 * kSubPerCta * kMtN) * 8);
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(mt_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr = true;
     }
-    mt_block_kernel<<<(unsigned)blocks, kMtThreads, smem, stream>>>(s.mt_seq, polys, len, ndraws, s.draws,
-                                                                    s.mt_windows, s.mt_reject);
-    mt_fixup_kernel<<<1, kMtThreads, 0, stream>>>(s.mt_windows, len, ndraws, s.draws, s.mt_reject);
+    const unsigned ctas = (unsigned)((nsub + kSubPerCta - 1) / kSubPerCta);
+    mt_block_kernel<<<ctas, kBlockThreads, smem, stream>>>(s.mt_seq, polys, W, nsub, len, ndraws, s.draws,
+                                                           s.mt_windows, s.mt_reject);
+    mt_fixup_kernel<<<1, kMtThreads, 0, stream>>>(s.mt_windows, W, len, ndraws, s.draws, s.mt_reject);
     cudaMemsetAsync(s.first, 0xff, len * sizeof(uint32_t), stream);
     cudaMemsetAsync(s.second, 0xff, len * sizeof(uint32_t), stream);
     first_pass<<<sm_grid(ndraws, 256), 256, 0, stream>>>(s.draws, len, ndraws, s.first);
