@@ -75,6 +75,7 @@ constexpr uint32_t OFF_G = 4 * BMAT;            // gradient tile (TMA, swizzled)
 constexpr uint32_t OFF_ST = OFF_G + TILE;       // p, exp_avg, exp_avg_sq staging tiles
 constexpr uint32_t OFF_SCR = OFF_ST + 3 * TILE; // merge grids (8 x 4 KB)
 constexpr uint32_t SCR_WARP = 4096;
+constexpr int kStageMax = 10;  // MASK_SIGN members staged per warp: 16 rows x (16 + 8) B each in SCR_WARP
 constexpr uint32_t OFF_BAR = OFF_SCR + kSelWarps * SCR_WARP;
 constexpr uint32_t OFF_L1 = OFF_BAR + 128;      // ||x||_1 per chunk, two tiles
 constexpr uint32_t SMEM_BYTES = OFF_L1 + 2 * TM * 4;
@@ -176,7 +177,7 @@ __device__ __forceinline__ void evt(const ChunkArgs& a, bool who, uint32_t it, i
   if (a.dbg && who && blockIdx.x == 0 && it < 32) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.dbg[it * 16 + id] = t;
+    a.dbg[it * 32 + id] = t;
   }
 }
 
@@ -187,7 +188,7 @@ __device__ __forceinline__ void evt_at(const ChunkArgs& a, bool who, uint32_t it
   if (a.dbg && who && blockIdx.x == 0 && it < 32) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.dbg[512 + it * 32 + slot] = t;
+    a.dbg[1024 + it * 32 + slot] = t;
   }
 }
 
@@ -562,6 +563,17 @@ __global__ void __maxnreg__(128)
     for (int v = 0; v < kLoads; ++v)
       tma_2d(smem + OFF_ST + v * TILE + h * BOX, m[v], 32 * h, (int)(t * TM), &bar_s[h]);
   };
+  // gradient tile t (and, SGD modes, the momentum tile) into the single gradient stage: issued
+  // by one thread of the apply warps once the front of the previous tile has consumed it
+  auto load_grad = [&](uint64_t t) {
+    mbar_arrive_expect_tx(bar_g, kMomentum ? 2 * TILE : TILE);
+    tma_2d(smem + OFF_G, &maps.g, 0, (int)(t * TM), bar_g);
+    tma_2d(smem + OFF_G + BOX, &maps.g, 32, (int)(t * TM), bar_g);
+    if (kMomentum) {  // the momentum tile: m_acc = beta m + g is the vector encoded
+      tma_2d(smem + OFF_M, &maps.ea_in, 0, (int)(t * TM), bar_g);
+      tma_2d(smem + OFF_M + BOX, &maps.ea_in, 32, (int)(t * TM), bar_g);
+    }
+  };
   // The two control warps stay converged: every lane runs the loop and the waits, lane 0
   // issues the TMA / tcgen05 operations.
   if (warp == kMemWarp) {
@@ -594,20 +606,8 @@ __global__ void __maxnreg__(128)
   }
 
   if (warp == kMmaWarp) {
-    // ===== MMA warp: gradient TMA and tcgen05.mma issue, in tile order =====
+    // ===== MMA warp: every tcgen05.mma, in tile order =====
     const uint32_t s_base = smem_u32(smem);
-    auto load_g = [&](uint64_t t) {
-      if (lane == 0) {
-        mbar_arrive_expect_tx(bar_g, kMomentum ? 2 * TILE : TILE);
-        tma_2d(smem + OFF_G, &maps.g, 0, (int)(t * TM), bar_g);
-        tma_2d(smem + OFF_G + BOX, &maps.g, 32, (int)(t * TM), bar_g);
-        if (kMomentum) {  // the momentum tile: m_acc = beta m + g is the vector encoded
-          tma_2d(smem + OFF_M, &maps.ea_in, 0, (int)(t * TM), bar_g);
-          tma_2d(smem + OFF_M + BOX, &maps.ea_in, 32, (int)(t * TM), bar_g);
-        }
-      }
-      __syncwarp();
-    };
     // D = A(TMEM: hi, lo) x B(smem hi, lo) in 3xTF32 over K = 64.  The 16 small
     // cross terms (hi*lo, lo*hi: |term| <= 2^-10 |x||B|) accumulate first and the 8 hi*hi
     // steps last, so the accumulator is small while the small terms are added: this is
@@ -644,18 +644,17 @@ __global__ void __maxnreg__(128)
       __syncwarp();
     };
     if (kFwd && tile < ntiles) {
-      load_g(tile);
       mbar_wait(bar_x, 0);
       issue(tmem + COL_C, OFF_BHI, OFF_BLO, bar_f);
-      if (tile + G < ntiles) load_g(tile + G);
     }
     for (uint32_t it = 0; tile < ntiles; tile += G, ++it) {
       const uint64_t t1 = tile + G;
       if (kFwd && t1 < ntiles) {
-        mbar_wait(bar_x, (it + 1) & 1);  // X of t+1 in TMEM; the gradient stage is free
+        mbar_wait(bar_x, (it + 1) & 1);  // X of t+1 in TMEM
+        evt(a, tid == 32 * kMmaWarp, it + 1, 18);
         mbar_wait(bar_c, it & 1);        // C of t read out by the select warps
+        evt(a, tid == 32 * kMmaWarp, it + 1, 19);
         issue(tmem + COL_C, OFF_BHI, OFF_BLO, bar_f);
-        if (t1 + G < ntiles) load_g(t1 + G);
       }
       if (!kEncodeOnly) {
         mbar_wait(bar_w, it & 1);
@@ -680,9 +679,13 @@ __global__ void __maxnreg__(128)
     const int trow = 32 * (warp & 3) + lane;
     const uint32_t tl = (uint32_t)(32 * (warp & 3)) << 16;
     const AdamScalars A = a.adam;
-    auto front = [&](uint64_t t, uint32_t n) {
-      evt(a, tid == 32 * kSelWarps, n, 2);
-      mbar_wait(bar_g, n & 1);
+    // part kFull: everything; kSplit: X hi / lo, ||x||_1, require_finite (then X may go to the
+    // forward MMA); kRing (SGD modes): m_acc into its two-tile ring, once the apply of the tile
+    // two behind has read the slot
+    enum : int { kFull = 0, kSplit = 1, kRing = 2 };
+    auto front = [&](uint64_t t, uint32_t n, int part) {
+      evt(a, tid == 32 * kSelWarps, n, part == kRing ? 16 : 2);
+      if (part != kRing) mbar_wait(bar_g, n & 1);
       float l1 = 0.f;
       bool fin = true;
 #pragma unroll
@@ -696,8 +699,10 @@ __global__ void __maxnreg__(128)
           x[4 * e + 2] = v.z;
           x[4 * e + 3] = v.w;
         }
+        if (part != kRing) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) fin = fin && isfinite(x[e]);
+          for (int e = 0; e < 16; ++e) fin = fin && isfinite(x[e]);
+        }
         if (kMomentum) {  // m_acc = beta m + g, multiply then add (optim.cpp:27)
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -708,10 +713,11 @@ __global__ void __maxnreg__(128)
             x[4 * e + 3] = __fadd_rn(__fmul_rn(a.sgd.beta, m.w), x[4 * e + 3]);
           }
         }
+        if (kMomentum && part != kSplit) tmem_st16(tmem + tl + COL_MACC + 64 * (n & 1) + 16 * h, x);  // m_acc
+        if (part == kRing) continue;
 #pragma unroll
         for (int e = 0; e < 16; ++e) l1 += fabsf(x[e]);
-        if (kMomentum) tmem_st16(tmem + tl + COL_MACC + 64 * (n & 1) + 16 * h, x);  // m_acc for the apply
-        else if (!kEncodeOnly) tmem_st16(tmem + tl + COL_G + 64 * (n % 3) + 16 * h, x);  // raw g for the apply
+        if (!kMomentum && !kEncodeOnly) tmem_st16(tmem + tl + COL_G + 64 * (n % 3) + 16 * h, x);  // raw g
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           hi[e] = tf32_hi(x[e]);
@@ -719,6 +725,11 @@ __global__ void __maxnreg__(128)
         }
         tmem_st16(tmem + tl + COL_XH + 16 * h, hi);
         tmem_st16(tmem + tl + COL_XL + 16 * h, x);
+      }
+      if (part == kRing) {
+        tmem_st_wait();
+        evt(a, tid == 32 * kSelWarps, n, 17);
+        return;
       }
       if (!fin) {  // require_finite (vec.cpp:7-16): the lowest offending index wins
         const float* gs = reinterpret_cast<const float*>(smem + OFF_G);
@@ -741,16 +752,36 @@ __global__ void __maxnreg__(128)
       }
       evt(a, tid == 32 * kSelWarps, n, 3);
     };
-    if (kFwd && tile < ntiles) front(tile, 0);
+    // the gradient stage is single: the next tile's TMA is issued once every apply warp is
+    // done with the current one
+    const bool lead = tid == 32 * kSelWarps;
+    auto next_grad = [&](uint64_t t) {
+      named_sync(1, kAppWarps * 32);
+      if (lead && t < ntiles) load_grad(t);
+    };
+    if (kFwd && tile < ntiles) {
+      if (lead) load_grad(tile);
+      front(tile, 0, kFull);
+      next_grad(tile + G);
+    }
     if (kFwd && tile + G < ntiles) {
       mbar_wait(bar_f, 0);  // X of the first tile consumed by its forward DCT
-      front(tile + G, 1);
+      front(tile + G, 1, kFull);
+      next_grad(tile + 2 * G);
     }
     for (uint32_t it = 0; tile < ntiles; tile += G, ++it) {
+      const bool ahead = kFwd && tile + 2 * G < ntiles;  // a front two tiles ahead
       if (!kEncodeOnly) {
       evt(a, tid == 32 * kSelWarps, it, 10);
       mbar_wait(bar_i, it & 1);
       evt(a, tid == 32 * kSelWarps, it, 11);
+      if (ahead) {
+        // the inverse of this tile has read W (the X columns): the front of tile t+2 goes
+        // first, so its forward DCT (and the selection of t+1 waiting on it) overlaps this apply
+        tc_fence_after();
+        front(tile + 2 * G, it + 2, kMomentum ? kSplit : kFull);
+        if (!kMomentum) next_grad(tile + 3 * G);
+      }
       mbar_wait(&bar_s[0], it & 1);
       mbar_wait(&bar_s[1], it & 1);
       tc_fence_after();
@@ -854,16 +885,16 @@ __global__ void __maxnreg__(128)
         }
       }
       evt(a, tid == 32 * kSelWarps, it, 13);
+      if (ahead && kMomentum) {  // m_acc of t+2 into the ring slot this apply has just read
+        front(tile + 2 * G, it + 2, kRing);
+        next_grad(tile + 3 * G);
       }
-      // AdamW first: its store frees the staging tile for the next tile's state load, which
-      // then runs under this front
-      if (kFwd && tile + 2 * G < ntiles) {
-        // the X columns are free once the inverse of this tile (or, encode only, the
-        // forward of the next) has read them
-        if (!kEncodeOnly) mbar_wait(bar_i, it & 1);
-        else mbar_wait(bar_f, (it + 1) & 1);
+      } else if (ahead) {
+        // encode only: the X columns are free once the forward of the next tile has read them
+        mbar_wait(bar_f, (it + 1) & 1);
         tc_fence_after();
-        front(tile + 2 * G, it + 2);
+        front(tile + 2 * G, it + 2, kFull);
+        next_grad(tile + 3 * G);
       }
     }
     goto teardown;
@@ -880,6 +911,27 @@ __global__ void __maxnreg__(128)
     const bool need_signs = sign_mode || dtype == DMB_TERNARY;
     const uint64_t nvals = nchunks * (uint64_t)k;
     uint8_t* scr = smem + OFF_SCR + warp * SCR_WARP;
+    // MASK_SIGN merges: the warp's 16 rows of every member (16 B of codes + the 8 B mask per
+    // row) into the scratch with cp.async; committed, waited for by the decode
+    bool prefetched = false;
+    auto stage_rows = [&](uint64_t* stg, uint64_t wrow) {
+      const int R = a.in.R;
+      for (int pr = lane; pr < R * 16; pr += 32) {
+        const int rr = pr >> 4, lr = pr & 15;
+        const uint64_t row = wrow + lr;
+        if (row < nfull) {
+          const uint8_t* src = a.in.body[rr] + nchunks * 8 + row * 16;
+          const uint8_t* msk = a.in.body[rr] + row * 8;
+          // 8-byte copies: the code region starts at 8 * nchunks, 16-byte aligned only for even nchunks
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(stg + 2 * pr)), "l"(src) : "memory");
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(stg + 2 * pr + 1)), "l"(src + 8)
+                       : "memory");
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(stg + 2 * R * 16 + pr)), "l"(msk)
+                       : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
 
     for (uint32_t it = 0; tile < ntiles; tile += G, ++it) {
       const uint64_t t1 = tile + G;
@@ -1068,34 +1120,28 @@ __global__ void __maxnreg__(128)
 #pragma unroll
           for (int e = 0; e < 16; ++e) gq0[e] = gq1[e] = 0.0f;
           if (vd == DMB_TERNARY) {
-            // codes by column: the thread's columns 8r + 2s + b sit at bits 16r + 4s + 2b
-            // up to 16 members: the warp's 16 rows of every member are copied into its scratch
-            // with cp.async at once (one memory latency), then decoded in member order
-            const unsigned long long* mko = reinterpret_cast<const unsigned long long*>(a.in.body[a.own_rank]);
-            const uint64_t om0 = act0 ? __ldg(mko + r0) : 0ull, om1 = act1 ? __ldg(mko + r1) : 0ull;
-            const bool staged = a.in.R <= 16;
-            uint64_t* stg = reinterpret_cast<uint64_t*>(scr);  // [member][row][lo, hi]
-            const uint64_t wrow = trow0 + base;
+            // codes by column: the thread's columns 8r + 2s + b sit at bits 16r + 4s + 2b.  Up to
+            // kStageMax members: the warp's 16 rows of every member (codes and masks) are copied
+            // into its scratch with cp.async -- for the NEXT tile right after this tile's decode,
+            // so the memory latency runs under the W store and the wait for the forward
+            const bool staged = a.in.R <= kStageMax;
+            uint64_t* stg = reinterpret_cast<uint64_t*>(scr);  // [member][row][lo, hi], then [member][row] mask
+            const int R = a.in.R;
+            if (staged && !prefetched) stage_rows(stg, trow0 + base);
             if (staged) {
-              for (int pr = lane; pr < a.in.R * 16; pr += 32) {
-                const int rr = pr >> 4, lr = pr & 15;
-                const uint64_t row = wrow + lr;
-                uint64_t* d = stg + 2 * pr;
-                if (row < nfull) {
-                  const uint8_t* src = a.in.body[rr] + nchunks * 8 + row * 16;
-                  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d)), "l"(src) : "memory");
-                  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + 1)), "l"(src + 8) : "memory");
-                }
-              }
-              asm volatile("cp.async.commit_group;" ::: "memory");
               asm volatile("cp.async.wait_group 0;" ::: "memory");
               __syncwarp();
             }
+            const int q0 = lane >> 2;
+            const uint64_t* smk = stg + 2 * R * 16;
+            const unsigned long long* mko = reinterpret_cast<const unsigned long long*>(a.in.body[a.own_rank]);
+            const uint64_t om0 = !act0 ? 0ull : (staged ? smk[a.own_rank * 16 + q0] : __ldg(mko + r0));
+            const uint64_t om1 = !act1 ? 0ull : (staged ? smk[a.own_rank * 16 + q0 + 8] : __ldg(mko + r1));
             // the member sum of codes is an integer per column: count it bit-parallel.  Per
             // 32-bit half-word of codes, each of its two 16-bit lanes (r & 1) accumulates
             // plus + (1 - minus) for the even (b = 0) and the odd (b = 1) column of the
             // thread, i.e. value + 1 per member; the values are exact in FP32 whatever the order
-            const int q = lane >> 2;
+            const int q = q0;
             constexpr uint32_t M = 0x00010001u;
             uint32_t ce[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, co[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
             const int s4 = 4 * s;
@@ -1122,7 +1168,7 @@ __global__ void __maxnreg__(128)
               if (chk_act) {
                 if (s < 2) {
                   const unsigned long long* mk = reinterpret_cast<const unsigned long long*>(a.in.body[rr]);
-                  bad |= __popcll(__ldg(mk + (s ? r1 : r0))) != k;
+                  bad |= __popcll(staged ? smk[rr * 16 + q0 + 8 * s] : __ldg(mk + (s ? r1 : r0))) != k;
                 } else {
                   constexpr uint64_t Z = 0x5555555555555555ull;
                   const uint64_t lo = s == 2 ? lo0 : lo1, hi = s == 2 ? hi0 : hi1;
@@ -1139,6 +1185,11 @@ __global__ void __maxnreg__(128)
               }
             }
             if (bad) atomicExch(&a.status->protocol_error, 1u);
+            if (staged) {
+              __syncwarp();  // every lane is done with the scratch: prefetch the next tile's rows
+              prefetched = has_next;
+              if (has_next) stage_rows(stg, t1 * TM + base);
+            }
             const int Rm = a.in.R;
 #pragma unroll
             for (int e = 0; e < 16; ++e) {  // element e = 2r + b: half-word r / 2, lane r & 1
@@ -1147,7 +1198,6 @@ __global__ void __maxnreg__(128)
               gq0[e] = act0 ? (float)((int)((c[i] >> sh) & 0xffffu) - Rm) : 0.0f;
               gq1[e] = act1 ? (float)((int)((c[4 + i] >> sh) & 0xffffu) - Rm) : 0.0f;
             }
-            if (staged) __syncwarp();  // the scratch is rewritten by the next tile
             sel0 = act0 ? gather16(om0, s) : 0u;
             sel1 = act1 ? gather16(om1, s) : 0u;
           } else {
@@ -1281,6 +1331,7 @@ __global__ void __maxnreg__(128)
         evt(a, tid == 0, it, 7);
         if (kFwd) {
           if (has_next) mbar_wait(bar_f, (it + 1) & 1);  // X of t+1 consumed: the columns take W
+          else if (it > 0) mbar_wait(bar_i, (it - 1) & 1);  // last tile: W of t-1 read by its inverse
         } else if (it > 0) {
           mbar_wait(bar_i, (it - 1) & 1);  // MergeSgd: W of t-1 read by its inverse
         }

@@ -668,3 +668,39 @@ def test_random_substream_replay_matches_oracle(oracle, monkeypatch, L, c):
         want = oracle.selected_indices(rep, step, 1, L)
         got = p.selected_indices(rep_to_cfg(rep), step, 1, L).cpu().numpy()
         assert np.array_equal(got, want.astype(np.int64)), step
+
+
+@pytest.mark.parametrize("tiles_per_cta,k", [(1, 64), (2, 64), (3, 64), (3, 32), (2, 8)])
+def test_tc_step_few_tiles_per_cta(oracle, tiles_per_cta, k):
+    """The last tile of a CTA stores W without a next forward to wait on: it must still wait for
+    the inverse of the tile before (full band k = s, whose selection is instant, raced here)."""
+    import ctypes as C
+
+    from paper_2502_06728_b200 import _capi
+    from paper_2502_06728_b200.core import _ptr, _stream, context
+
+    p = P()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    n = 64 * 128 * sms * tiles_per_cta
+    rng = np.random.default_rng(tiles_per_cta + k)
+    g = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    p0 = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    ea0 = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    es0 = (ea0.astype(np.float64) ** 2 * 4 + 1e-6).astype(np.float32)
+    rep = Rep(scheme=DEMO, chunk_size=64, top_k=k, compression=k / 64, sign_mode=True, seed=1234)
+    c = rep_to_cfg(rep).c()
+    o = p.OptimizerConfig(p.OptimizerKind.DecoupledAdamW).c()
+    gd, pd, ead, esd = dev(g), dev(p0), dev(ea0), dev(es0)
+    steps = C.c_uint64(9)
+    rc = _capi.lib.dmb_step_adamw_local(context().h, _ptr(gd), _ptr(pd), _ptr(pd), _ptr(ead), _ptr(ead), _ptr(esd),
+                                        _ptr(esd), C.byref(steps), n, C.byref(o), C.byref(c), 9, 0, 1e-3, None,
+                                        _stream())
+    assert rc == 0, _capi.lib.dmb_last_error()
+    p.status()
+    e = oracle.select_and_encode(g.astype(np.float64), rep, 9, 0)
+    q = oracle.decode_and_merge(rep, [e["values"]], [e["freq_indices"]], n, 9, 0)
+    pw, ew, sw = p0.astype(np.float64), ea0.astype(np.float64), es0.astype(np.float64)
+    oracle.adamw_apply(pw, ew, sw, 9, g.astype(np.float64), e["local_q"], q, 0.9, 0.999, 1e-8, 0.0, 1e-3)
+    chunk_close(host(ead), ew, 64, what="exp_avg")
+    chunk_close(host(esd), sw, 64, what="exp_avg_sq")
+    update_close(host(pd), pw, p0, 1e-3, 64)

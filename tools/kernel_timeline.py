@@ -7,8 +7,9 @@ with -DDMB_KERNEL_EVENTS (make -C paper_2502_06728_b200/csrc events).
 
 Event ids (demo_tc_adam.cu evt()): select 0 start, 1 forward done (C readable), 4 ||x||_1 ready,
 5 TopK done, 6 certified, 7 W computed, 8 X of t+1 consumed (W may be stored), 9 W stored;
-apply 2 front start, 3 front end, 10 apply wait start, 11 inverse done, 12 state staged, 13 apply
-done; MMA 14 W ready, 15 D of t-1 read.  Prints, per tile, each stamp relative to tile 0's
+apply 2 front start, 3 front end (X in TMEM), 16 / 17 m_acc ring write start / end (SGD modes),
+10 apply wait start, 11 inverse done, 12 state staged, 13 apply done; MMA 18 X in TMEM, 19 C of
+t-1 read (forward issued), 14 W ready, 15 D of t-1 read (inverse issued).  Prints, per tile, each stamp relative to tile 0's
 select start (us) and the tile period, then the mean of every gap over tiles 8..31.
 """
 from __future__ import annotations
@@ -31,7 +32,8 @@ from paper_2502_06728_b200.core import context  # noqa: E402
 
 NAMES = {0: "sel.start", 1: "sel.C", 4: "sel.l1", 5: "sel.topk", 6: "sel.cert", 7: "sel.W", 8: "sel.Xfree",
          9: "sel.Wst", 2: "app.front0", 3: "app.front1", 10: "app.wait", 11: "app.inv", 12: "app.state",
-         13: "app.done", 14: "mma.W", 15: "mma.Dfree"}
+         13: "app.done", 14: "mma.W", 15: "mma.Dfree", 16: "app.ring0", 17: "app.ring1", 18: "mma.X",
+         19: "mma.Cfree"}
 
 
 def main():
@@ -56,7 +58,7 @@ def main():
     g = torch.randn(L, device=dev) * 1e-3
     p = torch.randn(L, device=dev) * 0.02
     s1, s2 = torch.zeros(L, device=dev), torch.zeros(L, device=dev)
-    buf = torch.zeros(32 * 16 + 32 * 32, dtype=torch.int64, device=dev)
+    buf = torch.zeros(32 * 32 + 32 * 32, dtype=torch.int64, device=dev)
     steps = C.c_uint64(0)
 
     def chk(rc):
@@ -119,9 +121,9 @@ def main():
     lib.dmb_debug_events(None)
     P.status()
     ev = buf.cpu().numpy().astype(np.int64)
-    t = ev[: 32 * 16].reshape(32, 16)
+    t = ev[: 32 * 32].reshape(32, 32)
     base = t[0, 0]
-    ids = [i for i in (2, 3, 0, 1, 4, 5, 6, 7, 8, 9, 14, 15, 10, 11, 12, 13) if t[:, i].any()]
+    ids = [i for i in (2, 3, 18, 19, 0, 1, 4, 5, 6, 7, 8, 9, 14, 15, 10, 11, 12, 13, 16, 17) if t[:, i].any()]
     print(f"mode {a.mode}: L = {L} ({a.tiles_per_cta} tiles per CTA), step {e0.elapsed_time(e1):.3f} ms, "
           f"{e0.elapsed_time(e1) * 1e3 / a.tiles_per_cta:.2f} us per tile per CTA")
     print("tile " + " ".join(f"{NAMES[i]:>10s}" for i in ids) + "   period")
