@@ -77,7 +77,7 @@ constexpr uint32_t OFF_SCR = OFF_ST + 3 * TILE; // merge grids (8 x 4 KB)
 constexpr uint32_t SCR_WARP = 4096;
 constexpr int kStageMax = 10;  // MASK_SIGN members staged per warp: 16 rows x (16 + 8) B each in SCR_WARP
 constexpr uint32_t OFF_BAR = OFF_SCR + kSelWarps * SCR_WARP;
-constexpr uint32_t OFF_L1 = OFF_BAR + 128;      // ||x||_1 per chunk, two tiles
+constexpr uint32_t OFF_L1 = OFF_BAR + 256;      // ||x||_1 per chunk, two tiles
 constexpr uint32_t SMEM_BYTES = OFF_L1 + 2 * TM * 4;
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 
@@ -418,6 +418,15 @@ __device__ __forceinline__ float adam_ratio(float m1, float m2, const AdamScalar
   r = fmaf(r, fmaf(-d, r, 1.0f), r);
   return (m1 * A.inv_bc1) * r;
 }
+// the wire value of a SELECTED coefficient of a stored row: there every |c| is above the
+// certification radius, so with signs cond(c) = copysign(1, c) -- one bit operation
+template <int WIRE>
+__device__ __forceinline__ float wire_of(float c) {
+  if (WIRE == kWireSign) return __uint_as_float((__float_as_uint(c) & 0x80000000u) | 0x3f800000u);
+  return cond_w<WIRE>(c);
+}
+// all ones when bit e of m is set, else zero (e is a compile-time constant in the unrolled loops)
+__device__ __forceinline__ uint32_t bit_mask(uint32_t m, int e) { return (uint32_t)((int32_t)(m << (31 - e)) >> 31); }
 // exact TF32 split: hi keeps the top 10 mantissa bits, lo = x - hi is exact in FP32
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
@@ -503,7 +512,9 @@ __global__ void __maxnreg__(128)
   uint64_t* bar_a = bar_s + 2;  // [2] that half written back into the staging tile (apply warps)
   uint64_t* bar_c = bar_a + 2;  // coefficient tile read out of TMEM (select warps)
   uint64_t* bar_l = bar_c + 1;  // [2] ||x||_1 of tile n in l1buf[n & 1] (apply warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_l + 2);
+  uint64_t* bar_p = bar_l + 2;  // [2] MASK_SIGN encode: selection pieces of tile n in buffer n & 1 (select)
+  uint64_t* bar_q = bar_p + 2;  // [2] ... and that buffer written out as the payload (apply warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_q + 2);
   float* l1buf = reinterpret_cast<float*>(smem + OFF_L1);
 
   const int tid = threadIdx.x;
@@ -532,6 +543,10 @@ __global__ void __maxnreg__(128)
     mbar_init(&bar_s[1], 1);
     mbar_init(&bar_a[0], kAppWarps);
     mbar_init(&bar_a[1], kAppWarps);
+    mbar_init(&bar_p[0], kSelWarps);
+    mbar_init(&bar_p[1], kSelWarps);
+    mbar_init(&bar_q[0], kAppWarps);
+    mbar_init(&bar_q[1], kAppWarps);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, TMEM_COLS);
@@ -549,6 +564,14 @@ __global__ void __maxnreg__(128)
   const int k = a.geo.k;
   const bool full_band = k == S;
   uint64_t tile = blockIdx.x;
+  // MASK_SIGN encodes: the select warps hand each row's selection and signs (16 bits each per
+  // quad thread) to the apply warps, which assemble the u64 mask and the 2-bit code words (one
+  // thread per row) and store them -- the select warps are the bound of the encode pass.  The
+  // pieces live in the third staging slot, free in encode modes.
+  const bool pay_off = (kEncodeOnly || kEncSgd) && a.body != nullptr && a.geo.wire_mask != 0 &&
+                       mask_value_dtype(a.geo) == DMB_TERNARY;
+  uint32_t* pieces = reinterpret_cast<uint32_t*>(smem + OFF_ST + 2 * TILE);  // [2][TM][4]
+  uint8_t* pskip = smem + OFF_ST + 2 * TILE + 2 * TM * 16;                   // [2][TM] no payload here
 
   // the staging tile moves in two 32-column halves: the apply warps hand back the first
   // half early, so its store and the next tile's first-half load start under the second
@@ -759,6 +782,43 @@ __global__ void __maxnreg__(128)
       named_sync(1, kAppWarps * 32);
       if (lead && t < ntiles) load_grad(t);
     };
+    // MASK_SIGN payload of tile t (pay_off): row trow's mask and code words from the quad's
+    // pieces (thread s holds the columns 8r + 2s + b, r = 0..7, b = 0..1 of its elements 2r + b)
+    auto spread_pairs = [](uint32_t v) {  // 2-bit group r of v -> bits 8r, 8r + 1
+      uint64_t x = v & 0xffffu;
+      x = (x | (x << 24)) & 0x000000FF000000FFull;
+      x = (x | (x << 12)) & 0x000F000F000F000Full;
+      return (x | (x << 6)) & 0x0303030303030303ull;
+    };
+    auto spread_bits = [](uint32_t v) {  // bit i -> bit 2i
+      uint64_t x = v;
+      x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
+      x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
+      x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
+      x = (x | (x << 2)) & 0x3333333333333333ull;
+      return (x | (x << 1)) & 0x5555555555555555ull;
+    };
+    auto payload = [&](uint64_t t, uint32_t n) {
+      mbar_wait(&bar_p[n & 1], (n >> 1) & 1);
+      const uint64_t row = t * TM + trow;
+      if (!pskip[(n & 1) * TM + trow]) {
+        const uint4 v = *reinterpret_cast<const uint4*>(pieces + (n & 1) * (TM * 4) + trow * 4);
+        const uint32_t pw[4] = {v.x, v.y, v.z, v.w};
+        uint64_t mask = 0, neg = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          mask |= spread_pairs(pw[q]) << (2 * q);
+          neg |= spread_pairs(pw[q] & (pw[q] >> 16)) << (2 * q);  // selected and negative
+        }
+        const uint64_t pos = mask & ~neg;
+        const uint64_t lo = spread_bits((uint32_t)pos) | (spread_bits((uint32_t)neg) << 1);
+        const uint64_t hi = spread_bits((uint32_t)(pos >> 32)) | (spread_bits((uint32_t)(neg >> 32)) << 1);
+        reinterpret_cast<uint64_t*>(a.body)[row] = mask;
+        store_dense(a.body + nchunks * 8, row, lo, hi);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_q[n & 1]);
+    };
     if (kFwd && tile < ntiles) {
       if (lead) load_grad(tile);
       front(tile, 0, kFull);
@@ -889,12 +949,16 @@ __global__ void __maxnreg__(128)
         front(tile + 2 * G, it + 2, kRing);
         next_grad(tile + 3 * G);
       }
-      } else if (ahead) {
-        // encode only: the X columns are free once the forward of the next tile has read them
-        mbar_wait(bar_f, (it + 1) & 1);
-        tc_fence_after();
-        front(tile + 2 * G, it + 2, kFull);
-        next_grad(tile + 3 * G);
+      if (kEncSgd && pay_off) payload(tile, it);
+      } else {
+        if (ahead) {
+          // encode only: the X columns are free once the forward of the next tile has read them
+          mbar_wait(bar_f, (it + 1) & 1);
+          tc_fence_after();
+          front(tile + 2 * G, it + 2, kFull);
+          next_grad(tile + 3 * G);
+        }
+        if (pay_off) payload(tile, it);
       }
     }
     goto teardown;
@@ -1046,7 +1110,24 @@ __global__ void __maxnreg__(128)
         evt_at(a, lane == 0, it, 16 + warp);
         // ---- payload: indices ascending, then values (replicate.cpp:316-356); MASK layout:
         // one u64 mask per chunk, then the values (2-bit codes when signs travel) ----
-        if (a.body) {
+        if (pay_off) {
+          if (it >= 2) mbar_wait(&bar_q[it & 1], ((it - 2) >> 1) & 1);  // the buffer's last tile written out
+          uint32_t sg0 = 0, sg1 = 0;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            sg0 |= (__float_as_uint(c0[e]) >> 31) << e;
+            sg1 |= (__float_as_uint(c1[e]) >> 31) << e;
+          }
+          uint32_t* pb = pieces + (it & 1) * (TM * 4);
+          pb[row0 * 4 + s] = sel0 | (sg0 << 16);
+          pb[row1 * 4 + s] = sel1 | (sg1 << 16);
+          if (s == 0) {
+            pskip[(it & 1) * TM + row0] = !act0 || def0;  // the fix-up kernel writes a deferred row
+            pskip[(it & 1) * TM + row1] = !act1 || def1;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_p[it & 1]);
+        } else if (a.body) {
           const uint64_t q0m = spread(sel0, s), q1m = spread(sel1, s);
           uint64_t all0 = q0m, all1 = q1m;
           all0 |= shfl64(all0, (lane & 28) | ((lane + 1) & 3));
@@ -1285,38 +1366,38 @@ __global__ void __maxnreg__(128)
         const float* grid = reinterpret_cast<const float*>(scr);
         const int l0 = lane >> 2, l1 = l0 + 8;
         float w0[16], w1[16], u0[16], u1[16];  // SGD: u = W2 = wire on the selection
+        // selections as per-element bit masks: an inactive row has sel = 0, full band sel = all
+        // (so no per-element row tests); a deferred row is NaN-tagged below
+        const bool w1_all = kSgd && WIRE == kWireF32;
+        const uint32_t cs0 = (full_band && !w1_all) || kMergeSgd ? 0u : sel0;  // coef on the selection
+        const uint32_t cs1 = (full_band && !w1_all) || kMergeSgd ? 0u : sel1;
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int col = qcol(e, s);
-          const bool on0 = (sel0 >> e) & 1u, on1 = (sel1 >> e) & 1u;
+          const uint32_t m0 = bit_mask(sel0, e), m1 = bit_mask(sel1, e);
+          const uint32_t k0 = bit_mask(cs0, e), k1 = bit_mask(cs1, e);
+          const uint32_t b0 = __float_as_uint(c0[e]), b1 = __float_as_uint(c1[e]);
           float v0, v1;
           if (kMomentum) {
             // W1 = coef on the selection (local_q; k = s: unused, m_out = 0).  StepSgd: with a
             // fp32 wire W2 = W1, so Q = D1 (and k = s keeps every coefficient in W1); else
             // W2 = wire on the selection
-            const bool w1_all = kSgd && WIRE == kWireF32;
-            v0 = (on0 && (!full_band || w1_all)) ? c0[e] : 0.0f;
-            v1 = (on1 && (!full_band || w1_all)) ? c1[e] : 0.0f;
+            v0 = __uint_as_float(b0 & k0);
+            v1 = __uint_as_float(b1 & k1);
             if (kQ2) {
-              const float x0 = full_band || on0 ? cond_w<WIRE>(c0[e]) : 0.0f;
-              const float x1 = full_band || on1 ? cond_w<WIRE>(c1[e]) : 0.0f;
-              u0[e] = def0 ? __int_as_float(0x7fc00000) : (act0 ? x0 : 0.0f);
-              u1[e] = def1 ? __int_as_float(0x7fc00000) : (act1 ? x1 : 0.0f);
+              u0[e] = __uint_as_float(__float_as_uint(wire_of<WIRE>(c0[e])) & m0);
+              u1[e] = __uint_as_float(__float_as_uint(wire_of<WIRE>(c1[e])) & m1);
             }
           } else if (kMerge) {  // an inactive row has no selection and an empty grid row
             const float g0v = a.geo.wire_mask ? gq0[e] : grid[l0 * S + (col ^ ((l0 & 7) << 3))];
             const float g1v = a.geo.wire_mask ? gq1[e] : grid[l1 * S + (col ^ ((l1 & 7) << 3))];
             // MergeAdam: W = Q - local_q of the own selection; MergeSgd: W = grid / R (Q)
-            v0 = g0v * invR - ((!kMergeSgd && on0 && !full_band) ? c0[e] : 0.0f);
-            v1 = g1v * invR - ((!kMergeSgd && on1 && !full_band) ? c1[e] : 0.0f);
-          } else if (WIRE == kWireSign) {
-            // the selection is empty on an inactive row; on a stored (certified) row every
-            // selected |c| is above the radius, so cond(c) = copysign(1, c) there
-            v0 = on0 ? copysignf(1.0f, c0[e]) - (full_band ? 0.0f : c0[e]) : 0.0f;
-            v1 = on1 ? copysignf(1.0f, c1[e]) - (full_band ? 0.0f : c1[e]) : 0.0f;
+            v0 = g0v * invR - __uint_as_float(b0 & k0);
+            v1 = g1v * invR - __uint_as_float(b1 & k1);
           } else {
-            v0 = on0 ? cond_w<WIRE>(c0[e]) - (full_band ? 0.0f : c0[e]) : 0.0f;
-            v1 = on1 ? cond_w<WIRE>(c1[e]) - (full_band ? 0.0f : c1[e]) : 0.0f;
+            // W = wire - coef on the selection (k = s: W = wire)
+            v0 = __uint_as_float(__float_as_uint(wire_of<WIRE>(c0[e]) - __uint_as_float(b0 & k0)) & m0);
+            v1 = __uint_as_float(__float_as_uint(wire_of<WIRE>(c1[e]) - __uint_as_float(b1 & k1)) & m1);
           }
           w0[e] = v0;
           w1[e] = v1;
@@ -1324,19 +1405,13 @@ __global__ void __maxnreg__(128)
         if (__any_sync(kFull, def0 || def1)) {  // rare: NaN-tag the deferred rows
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            if (def0) w0[e] = __int_as_float(0x7fc00000);
-            if (def1) w1[e] = __int_as_float(0x7fc00000);
+            if (def0) w0[e] = u0[e] = __int_as_float(0x7fc00000);
+            if (def1) w1[e] = u1[e] = __int_as_float(0x7fc00000);
           }
         }
         evt(a, tid == 0, it, 7);
-        if (kFwd) {
-          if (has_next) mbar_wait(bar_f, (it + 1) & 1);  // X of t+1 consumed: the columns take W
-          else if (it > 0) mbar_wait(bar_i, (it - 1) & 1);  // last tile: W of t-1 read by its inverse
-        } else if (it > 0) {
-          mbar_wait(bar_i, (it - 1) & 1);  // MergeSgd: W of t-1 read by its inverse
-        }
-        evt(a, tid == 0, it, 8);
-        tc_fence_after();
+        // the TF32 split before any wait; W2 (its own columns, free once the inverse of t-1
+        // has read them) goes out first, W into the X columns once the forward of t+1 is done
         uint32_t r[32];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
@@ -1346,13 +1421,24 @@ __global__ void __maxnreg__(128)
           r[4 * (e >> 1) + (e & 1)] = __float_as_uint(h0);
           r[4 * (e >> 1) + 2 + (e & 1)] = __float_as_uint(h1);
         }
+        if (kQ2) {  // W2 is TF32-exact (signs, fp16-rounded values): hi columns only
+          if (it > 0) mbar_wait(bar_i, (it - 1) & 1);
+          tc_fence_after();
+          uint32_t r2[32];
+          pack_rows(u0, u1, r2);
+          st_quad(tmem + tq + COL_W2H, r2);
+        }
+        if (kFwd) {
+          if (has_next) mbar_wait(bar_f, (it + 1) & 1);  // X of t+1 consumed: the columns take W
+          else if (it > 0) mbar_wait(bar_i, (it - 1) & 1);  // last tile: W of t-1 read by its inverse
+        } else if (it > 0) {
+          mbar_wait(bar_i, (it - 1) & 1);  // MergeSgd: W of t-1 read by its inverse
+        }
+        evt(a, tid == 0, it, 8);
+        tc_fence_after();
         st_quad(tmem + tq + COL_XH, r);
         pack_rows(w0, w1, r);
         st_quad(tmem + tq + COL_XL, r);
-        if (kQ2) {  // W2 is TF32-exact (signs, fp16-rounded values): hi columns only
-          pack_rows(u0, u1, r);
-          st_quad(tmem + tq + COL_W2H, r);
-        }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();

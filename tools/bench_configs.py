@@ -256,7 +256,7 @@ def main():
                       dtype=P.TransferDtype.Ternary)
         run(rank_step, L7, 1, 8, P.Scheme.DiLoCo, P.OptimizerKind.DemoSgd, max(3, S // 2), 2,
                   "config5 OLMo-2-7B 1x8 DiLoCo off-beat step (one rank)", compression=1.0 / 16, sign=True,
-                  diloco_offbeat=True)
+                  dtype=P.TransferDtype.Ternary, diloco_offbeat=True)
 
 
 if __name__ == "__main__":
