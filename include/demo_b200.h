@@ -67,9 +67,10 @@ enum { DMB_DEMO_SGD = 0, DMB_DECOUPLED_ADAMW = 1 };
 /* DeMo body layout.  REFERENCE: replicate.cpp:316-356 (u32 indices, then values per dtype).
  * MASK (exchange-only, lossless): one u64 frequency mask per chunk (bit j = frequency j),
  * then the values in ascending frequency per chunk, packed per dtype; MASK_SIGN (sign_mode
- * or ternary: the values are exactly -1/0/+1): the masks, then per chunk 2-bit codes by
- * column (16 bytes, 0 where not selected).  At s=64, k=32, sign on the body is 24 B per
- * chunk instead of 256 B.  dmb_serialize always emits the reference bytes. */
+ * or ternary: the values are exactly -1/0/+1): the masks, then per chunk 16 bytes of 2-bit
+ * codes (1: +1, 2: -1, 0: zero or not selected) as four u32 words, word s holding the
+ * frequencies 8r + 2s + b (r = 0..7, b = 0..1) at bits 2(2r + b).  At s=64, k=32, sign on the
+ * body is 24 B per chunk instead of 256 B.  dmb_serialize always emits the reference bytes. */
 enum { DMB_WIRE_REFERENCE = 0, DMB_WIRE_MASK = 1, DMB_WIRE_MASK_SIGN = 2 /* MASK, 2-bit values */ };
 
 /* ReplicatorConfig, replicate.hpp:28-39 */

@@ -349,15 +349,32 @@ class HybridCluster:
             lib.dmb_set_wire_format(ctx, 0)
         self.mask_wire = any(b["format"] for b in self.buckets)
         self.payload_bytes_per_param = (sum(b["bytes"] for b in self.buckets) / L) if L else 0.0
-        gathered = R * sum(b["xfer"] for b in self.buckets)
-        budget = int(os.environ.get("DMB_GATHER_BUDGET", "0")) or None
-        if budget is not None and gathered > budget:
-            raise ConfigError(f"the step holds {gathered} gathered payload bytes, above DMB_GATHER_BUDGET={budget}")
+        # memory: every bucket's own slot(s) and R gathered copies stay resident through a step;
+        # above the budget (DMB_GATHER_BUDGET bytes, default a quarter of the device) the step runs
+        # the buckets in windows that fit, after a finiteness pre-check of the whole shard that
+        # the ranks agree on first (one extra read of the gradient), so a refused step still
+        # changes nothing
+        self.window = len(self.buckets)
+        if R > 1 and self.buckets and not self.fused:
+            budget = int(os.environ.get("DMB_GATHER_BUDGET", "0")) or int(
+                0.25 * torch.cuda.get_device_properties(self.device).total_memory)
+            per = (R + 2) * max(b["xfer"] for b in self.buckets)
+            if per * len(self.buckets) > budget:
+                self.window = max(1, budget // per)
         if exchange is None:
             exchange = self._default_exchange(shard_group, replica_group, world_group)
+        if self.window < len(self.buckets):
+            if isinstance(exchange, LocalExchange):
+                raise ConfigError("the bucket windows of a memory-bounded step need a collective exchange")
+            if isinstance(exchange, CopyEngineExchange):  # slots are reused within a step: stream-ordered NCCL
+                exchange = CollectiveExchange(shard_group, replica_group, world_group, R, A)
         self.exchange = exchange
         if self.buckets and not self.fused:
-            exchange.setup([b["xfer"] for b in self.buckets], self.device)
+            if self.window < len(self.buckets):
+                mx = max(b["xfer"] for b in self.buckets)
+                exchange.setup([mx] * self.window, self.device)
+            else:
+                exchange.setup([b["xfer"] for b in self.buckets], self.device)
         self.ce = exchange if isinstance(exchange, CopyEngineExchange) else None
         if isinstance(exchange, LocalExchange):
             exchange.hub.members[rank] = self
@@ -391,6 +408,9 @@ class HybridCluster:
         c, o = self.rep.c(), self.opt.c()
         if self.fused:
             self._fused(ctx, c, o, st)
+        elif self.window < len(self.buckets):
+            self._windowed(ctx, c, o, st)
+            return
         else:
             self.exchange.begin_step()
             lib.dmb_set_wire_format(ctx, 1 if self.wire == "mask" else 0)
@@ -419,7 +439,9 @@ class HybridCluster:
         _check(lib.dmb_latch_export(ctx, _ptr(self.flag), st))
 
     def agree(self) -> None:
-        self.exchange.agree(self.flag)
+        if not getattr(self, "_agreed", False):
+            self.exchange.agree(self.flag)
+        self._agreed = False
 
     def commit(self, check: bool = True) -> StepTraffic:
         """merges + applies (no-ops on a refused step), status, buffer swaps"""
@@ -429,7 +451,7 @@ class HybridCluster:
             ctx = context(self.device).h
             st = _stream(self.g_shard)
             _check(lib.dmb_latch_import(ctx, _ptr(self.flag), st))
-            if not self.fused:
+            if not self.fused and self._pending:
                 c, o = self.rep.c(), self.opt.c()
                 R = self.topo.nodes
                 steps = C.c_uint64(self.steps)
@@ -476,6 +498,73 @@ class HybridCluster:
             raise
 
     # ---- internals ----------------------------------------------------------------
+    def _prepare(self, ctx, c, o, st, bi, slot):
+        """one bucket's prepare into exchange slot `slot`; returns its header"""
+        b = self.buckets[bi]
+        lo, hi = b["lo"], b["hi"]
+        hdr = _capi.Update()
+        hdr.body = self.exchange.own(slot).data_ptr()
+        if self.sgd:
+            _check(lib.dmb_demo_sgd_prepare(ctx, _ptr(self.g_shard[lo:hi]), _ptr(self.m[lo:hi]),
+                                            _ptr(self._m_next[lo:hi]), hi - lo, C.byref(o), C.byref(c), self._step,
+                                            self.accel, C.byref(hdr), None, None, st))
+        else:
+            _check(lib.dmb_adamw_prepare(ctx, _ptr(self.g_shard[lo:hi]), hi - lo, C.byref(c), self._step, self.accel,
+                                         C.byref(hdr), None, st))
+        if not hdr.empty and (int(hdr.wire_format) != b["format"] or int(hdr.bytes) > self.exchange.xfers[slot]):
+            raise ProtocolError(f"bucket {bi}: the prepare produced layout {hdr.wire_format} / {hdr.bytes} B, "
+                                f"planned {b['format']} / {self.exchange.xfers[slot]} B")
+        R = self.topo.nodes
+        self._tr.inter_bytes += int(hdr.bytes) * (R - 1)  # cluster.cpp:212
+        self._tr.inter_bytes_reference += int(lib.dmb_wire_bytes(hdr.n_values, hdr.n_indices,
+                                                                  self.rep.transfer_dtype)) * (R - 1)
+        return hdr
+
+    def _merge(self, ctx, c, o, st, bi, hdr, ptrs):
+        b = self.buckets[bi]
+        lo, hi = b["lo"], b["hi"]
+        R = self.topo.nodes
+        ups, n_up = None, 0
+        if ptrs is not None:
+            ups = (_capi.Update * R)()
+            for r in range(R):
+                ups[r] = hdr
+                ups[r].body = ptrs[r]
+            n_up = R
+        if self.sgd:
+            _check(lib.dmb_merge_apply_sgd(ctx, ups, n_up, C.byref(c), _ptr(self.params[lo:hi]),
+                                           _ptr(self.g_shard[lo:hi]), hi - lo, self._step, self._lr, st))
+        else:
+            steps = C.c_uint64(self._steps0)  # every bucket advances the counter from the same value
+            _check(lib.dmb_merge_apply_adamw(ctx, ups, n_up, self.node, C.byref(c), _ptr(self.params[lo:hi]),
+                                             _ptr(self.exp_avg[lo:hi]), _ptr(self.exp_avg_sq[lo:hi]), C.byref(steps),
+                                             _ptr(self.g_shard[lo:hi]), hi - lo, self._step, C.byref(o), self._lr,
+                                             st))
+
+    def _windowed(self, ctx, c, o, st) -> None:
+        """memory-bounded step: agree on the finiteness of the whole shard first, then prepare,
+        exchange and merge the buckets `window` at a time through the reused slots"""
+        L = self.spec.real_len
+        _check(lib.dmb_require_finite(ctx, _ptr(self.g_shard), L, st))
+        _check(lib.dmb_latch_export(ctx, _ptr(self.flag), st))
+        self.exchange.agree(self.flag)
+        _check(lib.dmb_latch_import(ctx, _ptr(self.flag), st))
+        self._agreed = True
+        lib.dmb_set_wire_format(ctx, 1 if self.wire == "mask" else 0)
+        try:
+            nb, W = len(self.buckets), self.window
+            for w0 in range(0, nb, W):
+                win = []
+                for bi in range(w0, min(nb, w0 + W)):
+                    hdr = self._prepare(ctx, c, o, st, bi, bi - w0)
+                    win.append((bi, hdr, self.exchange.start(bi - w0) if not hdr.empty else None))
+                for bi, hdr, handle in win:
+                    self._merge(ctx, c, o, st, bi, hdr, None if hdr.empty else self.exchange.bodies(bi - w0, handle))
+        finally:
+            lib.dmb_set_wire_format(ctx, 0)
+        if not self.sgd:
+            self.steps = self._steps0 + 1
+
     def _swap(self) -> None:
         if not self.spec.real_len:
             return

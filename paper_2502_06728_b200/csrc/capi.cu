@@ -729,8 +729,10 @@ int dmb_serialize(const dmb_update* u, int32_t dtype, uint8_t* host_out, uint64_
         if (!(mk & 1)) continue;
         std::memcpy(idx + 4 * t, &j, 4);
         float v;
-        if (vd == DMB_TERNARY) {  // codes by column: 16 bytes per chunk
-          const uint32_t code = (vin[16 * c + (j >> 2)] >> (2 * (j & 3))) & 3u;
+        if (vd == DMB_TERNARY) {  // quad-order code words: 16 bytes per chunk
+          uint32_t word;
+          std::memcpy(&word, vin + 16 * c + 4 * ((j >> 1) & 3), 4);
+          const uint32_t code = (word >> (2 * (2 * (j >> 3) + (j & 1)))) & 3u;
           v = code == 1u ? 1.0f : (code == 2u ? -1.0f : 0.0f);
         } else if (vd == DMB_FP16) {
           uint16_t h;

@@ -430,14 +430,25 @@ __device__ __forceinline__ uint32_t bit_mask(uint32_t m, int e) { return (uint32
 // exact TF32 split: hi keeps the top 10 mantissa bits, lo = x - hi is exact in FP32
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
-// MASK bodies with signs (DMB_WIRE_MASK_SIGN): after the masks, each chunk's 2-bit codes by
-// column (code 1: +1, 2: -1, 0: zero or not selected), columns 0-31 in the first u64, 32-63
-// in the second -- decoding is a shift per column, independent of k
+// MASK bodies with signs (DMB_WIRE_MASK_SIGN): after the masks, each chunk's 2-bit codes
+// (code 1: +1, 2: -1, 0: zero or not selected) in QUAD ORDER -- four u32 words per chunk, word
+// s holding the 16 columns 8r + 2s + b (r = 0..7, b = 0..1) at bits 2(2r + b): exactly the
+// columns one quad thread of the tensor-core kernels holds, so a thread encodes and decodes
+// its own word, and the merge accumulates all 16 of its columns with a few bit operations per
+// member (include/demo_b200.h states the layout; dmb_serialize expands it)
 __device__ __forceinline__ uint32_t code_of(float w) { return w > 0.0f ? 1u : (w < 0.0f ? 2u : 0u); }
 __device__ __forceinline__ float value_of(uint32_t code) { return code == 1u ? 1.0f : (code == 2u ? -1.0f : 0.0f); }
-__device__ __forceinline__ void store_dense(uint8_t* vals, uint64_t row, uint64_t lo, uint64_t hi) {
-  reinterpret_cast<uint64_t*>(vals)[2 * row] = lo;
-  reinterpret_cast<uint64_t*>(vals)[2 * row + 1] = hi;
+// 16 bits -> bits 2i (Morton spread of one operand)
+__device__ __forceinline__ uint32_t spread16(uint32_t x) {
+  x &= 0xffffu;
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  return (x | (x << 1)) & 0x55555555u;
+}
+// a thread's code word from its selection and sign bits (element e at bits 2e)
+__device__ __forceinline__ uint32_t code_word(uint32_t sel, uint32_t neg) {
+  return spread16(sel & ~neg) | (spread16(sel & neg) << 1);
 }
 
 // selection of a row from its threshold masks (gt: |c| > T, eq: |c| == T): everything
@@ -790,31 +801,19 @@ __global__ void __maxnreg__(128)
       x = (x | (x << 12)) & 0x000F000F000F000Full;
       return (x | (x << 6)) & 0x0303030303030303ull;
     };
-    auto spread_bits = [](uint32_t v) {  // bit i -> bit 2i
-      uint64_t x = v;
-      x = (x | (x << 16)) & 0x0000FFFF0000FFFFull;
-      x = (x | (x << 8)) & 0x00FF00FF00FF00FFull;
-      x = (x | (x << 4)) & 0x0F0F0F0F0F0F0F0Full;
-      x = (x | (x << 2)) & 0x3333333333333333ull;
-      return (x | (x << 1)) & 0x5555555555555555ull;
-    };
     auto payload = [&](uint64_t t, uint32_t n) {
       mbar_wait(&bar_p[n & 1], (n >> 1) & 1);
       const uint64_t row = t * TM + trow;
       if (!pskip[(n & 1) * TM + trow]) {
         const uint4 v = *reinterpret_cast<const uint4*>(pieces + (n & 1) * (TM * 4) + trow * 4);
         const uint32_t pw[4] = {v.x, v.y, v.z, v.w};
-        uint64_t mask = 0, neg = 0;
+        uint64_t mask = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          mask |= spread_pairs(pw[q]) << (2 * q);
-          neg |= spread_pairs(pw[q] & (pw[q] >> 16)) << (2 * q);  // selected and negative
-        }
-        const uint64_t pos = mask & ~neg;
-        const uint64_t lo = spread_bits((uint32_t)pos) | (spread_bits((uint32_t)neg) << 1);
-        const uint64_t hi = spread_bits((uint32_t)(pos >> 32)) | (spread_bits((uint32_t)(neg >> 32)) << 1);
+        for (int q = 0; q < 4; ++q) mask |= spread_pairs(pw[q]) << (2 * q);
         reinterpret_cast<uint64_t*>(a.body)[row] = mask;
-        store_dense(a.body + nchunks * 8, row, lo, hi);
+        uint32_t* cw = reinterpret_cast<uint32_t*>(a.body + nchunks * 8) + 4 * row;  // quad order
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cw[q] = code_word(pw[q] & 0xffffu, pw[q] >> 16);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_q[n & 1]);
@@ -1143,38 +1142,18 @@ __global__ void __maxnreg__(128)
             if (act1 && !def1) reinterpret_cast<uint64_t*>(a.body)[r1] = all1;
           }
           const bool words = mask_wire && vd == DMB_TERNARY;
-          if (words) {  // the rows' codes by column, assembled across the quad
-            // element e = 2r + b of this thread is column 8r + 2s + b: its code goes to bit
-            // 16(r & 1) + 2b + 4s of 32-bit word r / 2 (columns 16(r / 2) .. +15). A stored row
-            // has every selected |c| above the certification radius, so c != 0 there and its
-            // code is 1 + the sign bit
-            uint32_t w0[4] = {0u, 0u, 0u, 0u}, w1[4] = {0u, 0u, 0u, 0u};
+          if (words) {  // each thread's own code word of both rows (quad order)
+            // a stored row has every selected |c| above the certification radius, so c != 0
+            // there and its code is 1 + the sign bit
+            uint32_t sg0 = 0, sg1 = 0;
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
-              const int sh = 16 * ((e >> 1) & 1) + 2 * (e & 1);
-              w0[e >> 2] += (((sel0 >> e) & 1u) * (1u + (__float_as_uint(c0[e]) >> 31))) << sh;
-              w1[e >> 2] += (((sel1 >> e) & 1u) * (1u + (__float_as_uint(c1[e]) >> 31))) << sh;
+              sg0 |= (__float_as_uint(c0[e]) >> 31) << e;
+              sg1 |= (__float_as_uint(c1[e]) >> 31) << e;
             }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              w0[q] <<= 4 * s;
-              w1[q] <<= 4 * s;
-            }
-#pragma unroll
-            for (int o = 1; o <= 2; ++o) {
-              const int src = (lane & 28) | ((lane + o) & 3);
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                w0[q] |= __shfl_sync(kFull, w0[q], src);
-                w1[q] |= __shfl_sync(kFull, w1[q], src);
-              }
-            }
-            const uint64_t l0 = w0[0] | ((uint64_t)w0[1] << 32), h0 = w0[2] | ((uint64_t)w0[3] << 32);
-            const uint64_t l1 = w1[0] | ((uint64_t)w1[1] << 32), h1 = w1[2] | ((uint64_t)w1[3] << 32);
-            if (s == 0) {
-              if (act0 && !def0) store_dense(vals, r0, l0, h0);
-              if (act1 && !def1) store_dense(vals, r1, l1, h1);
-            }
+            uint32_t* cw = reinterpret_cast<uint32_t*>(vals);
+            if (act0 && !def0) cw[4 * r0 + s] = code_word(sel0, sg0);
+            if (act1 && !def1) cw[4 * r1 + s] = code_word(sel1, sg1);
           }
 #pragma unroll
           for (int e = 0; e < 16 && !words; ++e) {
@@ -1218,51 +1197,38 @@ __global__ void __maxnreg__(128)
             const unsigned long long* mko = reinterpret_cast<const unsigned long long*>(a.in.body[a.own_rank]);
             const uint64_t om0 = !act0 ? 0ull : (staged ? smk[a.own_rank * 16 + q0] : __ldg(mko + r0));
             const uint64_t om1 = !act1 ? 0ull : (staged ? smk[a.own_rank * 16 + q0 + 8] : __ldg(mko + r1));
-            // the member sum of codes is an integer per column: count it bit-parallel.  Per
-            // 32-bit half-word of codes, each of its two 16-bit lanes (r & 1) accumulates
-            // plus + (1 - minus) for the even (b = 0) and the odd (b = 1) column of the
-            // thread, i.e. value + 1 per member; the values are exact in FP32 whatever the order
-            const int q = q0;
-            constexpr uint32_t M = 0x00010001u;
-            uint32_t ce[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, co[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-            const int s4 = 4 * s;
-            // protocol checks (replicate.cpp:284-293 for this layout), split over the quad: threads
-            // 0 / 1 check that the member's mask of row 0 / 1 selects exactly k frequencies,
-            // threads 2 / 3 that the row's code words hold no invalid code 3 and at most k
-            // nonzero codes
+            // the member sum of codes is an integer per column: count it bit-parallel.  In the
+            // thread's own code word (quad order), plus + (1 - minus) = value + 1 in {0, 1, 2} per
+            // 2-bit field; four byte-lane accumulators take fields e = j (mod 4) at byte e / 4, so
+            // each member costs a few bit operations for all 16 columns of a row (R <= 64: a
+            // byte holds 2R); the values are exact in FP32 whatever the order
+            constexpr uint32_t H = 0x55555555u, B = 0x03030303u;
+            uint32_t a0[4] = {0u, 0u, 0u, 0u}, a1[4] = {0u, 0u, 0u, 0u};
+            // protocol checks (replicate.cpp:284-293 for this layout): every member's mask of an
+            // active row selects exactly k frequencies (threads 0 / 1 for rows 0 / 1) and no code
+            // word holds the invalid code 3
             bool bad = false;
-            const bool chk_act = (s & 1) ? act1 : act0;
+            const uint32_t* st32 = reinterpret_cast<const uint32_t*>(stg);
             for (int rr = 0; rr < a.in.R; ++rr) {
-              uint64_t lo0, hi0, lo1, hi1;
+              uint32_t v0, v1;
               if (staged) {
-                lo0 = act0 ? stg[2 * (rr * 16 + q)] : 0ull;
-                hi0 = act0 ? stg[2 * (rr * 16 + q) + 1] : 0ull;
-                lo1 = act1 ? stg[2 * (rr * 16 + q + 8)] : 0ull;
-                hi1 = act1 ? stg[2 * (rr * 16 + q + 8) + 1] : 0ull;
+                v0 = act0 ? st32[4 * (rr * 16 + q0) + s] : 0u;  // an inactive row's grid is zeroed below
+                v1 = act1 ? st32[4 * (rr * 16 + q0 + 8) + s] : 0u;
               } else {
-                const unsigned long long* dv = reinterpret_cast<const unsigned long long*>(a.in.body[rr] + nchunks * 8);
-                lo0 = act0 ? __ldg(dv + 2 * r0) : 0ull;
-                hi0 = act0 ? __ldg(dv + 2 * r0 + 1) : 0ull;
-                lo1 = act1 ? __ldg(dv + 2 * r1) : 0ull;
-                hi1 = act1 ? __ldg(dv + 2 * r1 + 1) : 0ull;
+                const uint32_t* dv = reinterpret_cast<const uint32_t*>(a.in.body[rr] + nchunks * 8);
+                v0 = act0 ? __ldg(dv + 4 * r0 + s) : 0u;
+                v1 = act1 ? __ldg(dv + 4 * r1 + s) : 0u;
               }
-              if (chk_act) {
-                if (s < 2) {
-                  const unsigned long long* mk = reinterpret_cast<const unsigned long long*>(a.in.body[rr]);
-                  bad |= __popcll(staged ? smk[rr * 16 + q0 + 8 * s] : __ldg(mk + (s ? r1 : r0))) != k;
-                } else {
-                  constexpr uint64_t Z = 0x5555555555555555ull;
-                  const uint64_t lo = s == 2 ? lo0 : lo1, hi = s == 2 ? hi0 : hi1;
-                  bad |= (((lo & (lo >> 1)) | (hi & (hi >> 1))) & Z) != 0ull;
-                  bad |= __popcll((lo | (lo >> 1)) & Z) + __popcll((hi | (hi >> 1)) & Z) > k;
-                }
+              if (s < 2 && (s ? act1 : act0)) {
+                const unsigned long long* mk = reinterpret_cast<const unsigned long long*>(a.in.body[rr]);
+                bad |= __popcll(staged ? smk[rr * 16 + q0 + 8 * s] : __ldg(mk + (s ? r1 : r0))) != k;
               }
-              const uint32_t w[8] = {(uint32_t)lo0, (uint32_t)(lo0 >> 32), (uint32_t)hi0, (uint32_t)(hi0 >> 32),
-                                     (uint32_t)lo1, (uint32_t)(lo1 >> 32), (uint32_t)hi1, (uint32_t)(hi1 >> 32)};
+              bad |= (((v0 & (v0 >> 1)) | (v1 & (v1 >> 1))) & H) != 0u;
+              const uint32_t t0 = (v0 & H) + (~(v0 >> 1) & H), t1v = (v1 & H) + (~(v1 >> 1) & H);
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                ce[i] += ((w[i] >> s4) & M) + (~(w[i] >> (s4 + 1)) & M);
-                co[i] += ((w[i] >> (s4 + 2)) & M) + (~(w[i] >> (s4 + 3)) & M);
+              for (int j = 0; j < 4; ++j) {
+                a0[j] += (t0 >> (2 * j)) & B;
+                a1[j] += (t1v >> (2 * j)) & B;
               }
             }
             if (bad) atomicExch(&a.status->protocol_error, 1u);
@@ -1273,11 +1239,9 @@ __global__ void __maxnreg__(128)
             }
             const int Rm = a.in.R;
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {  // element e = 2r + b: half-word r / 2, lane r & 1
-              const int r = e >> 1, i = r >> 1, sh = 16 * (r & 1);
-              const uint32_t* c = (e & 1) ? co : ce;
-              gq0[e] = act0 ? (float)((int)((c[i] >> sh) & 0xffffu) - Rm) : 0.0f;
-              gq1[e] = act1 ? (float)((int)((c[4 + i] >> sh) & 0xffffu) - Rm) : 0.0f;
+            for (int e = 0; e < 16; ++e) {  // element e: accumulator e & 3, byte e >> 2
+              gq0[e] = act0 ? (float)((int)((a0[e & 3] >> (8 * (e >> 2))) & 0xffu) - Rm) : 0.0f;
+              gq1[e] = act1 ? (float)((int)((a1[e & 3] >> (8 * (e >> 2))) & 0xffu) - Rm) : 0.0f;
             }
             sel0 = act0 ? gather16(om0, s) : 0u;
             sel1 = act1 ? gather16(om1, s) : 0u;
@@ -1648,12 +1612,20 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
       uint32_t* idx = reinterpret_cast<uint32_t*>(a.body);
       uint8_t* vals = a.body + (mask_wire ? a.geo.nchunks * 8 : nvals * 4);
       if (mask_wire && lane == 0) reinterpret_cast<uint64_t*>(a.body)[c] = ((uint64_t)m1 << 32) | m0;
-      if (mask_wire && vd == DMB_TERNARY) {  // codes by column: lane j holds columns j and j+32
-        const uint64_t lo = sel0 ? (uint64_t)code_of(w0) << (2 * lane) : 0ull;
-        const uint64_t hi = sel1 ? (uint64_t)code_of(w1) << (2 * lane) : 0ull;
-        const uint64_t l = ((uint64_t)__reduce_or_sync(kFull, (uint32_t)(lo >> 32)) << 32) | __reduce_or_sync(kFull, (uint32_t)lo);
-        const uint64_t h = ((uint64_t)__reduce_or_sync(kFull, (uint32_t)(hi >> 32)) << 32) | __reduce_or_sync(kFull, (uint32_t)hi);
-        if (lane == 0) store_dense(vals, c, l, h);
+      if (mask_wire && vd == DMB_TERNARY) {  // quad-order code words: lane j holds columns j and j+32
+        // column col sits in word (col >> 1) & 3 at bits 2e, e = 2 (col >> 3) + (col & 1)
+        uint32_t wv[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = lane + 32 * h;
+          const uint32_t code = (h ? sel1 : sel0) ? code_of(h ? w1 : w0) : 0u;
+          const int e = 2 * (col >> 3) + (col & 1);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) wv[q] |= (((col >> 1) & 3) == q) ? code << (2 * e) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) wv[q] = __reduce_or_sync(kFull, wv[q]);
+        if (lane < 4) reinterpret_cast<uint32_t*>(vals)[4 * c + lane] = wv[lane];
       } else {
       if (sel0) {
         const uint64_t t = c * (uint64_t)k + __popc(m0 & lt);
