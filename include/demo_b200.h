@@ -227,6 +227,33 @@ int dmb_grad_mean(dmb_ctx* ctx, const float* const* grads, uint64_t members, uin
 /* require_finite (vec.cpp:7-16) on its own: latches the first non-finite index */
 int dmb_require_finite(dmb_ctx* ctx, const float* v, uint64_t n, void* stream);
 
+/* ---- model.hpp: the toy gradient producers, for the trainer loop (trainer.cpp:49-90) ----
+ * dmb_toy_model mirrors Model (model.hpp:36-46): kind 0 quadratic (dims = {dim}), 1 mlp
+ * (dims = layer_dims, at most 9 entries); activation 0 tanh / 1 relu; loss 0 mse / 1 cross
+ * entropy.  dmb_toy_pool is a dataset split resident on the device (dataset.hpp:18-23). */
+typedef struct dmb_toy_model {
+  uint32_t kind, activation, loss, n_dims;
+  uint32_t dims[9];
+} dmb_toy_model;
+typedef struct dmb_toy_pool {
+  const double* inputs;   /* size x dims[0] */
+  const double* targets;  /* size x dims[n_dims-1] (mse), or NULL */
+  const int32_t* labels;  /* size (cross entropy), or NULL */
+  uint64_t size;
+} dmb_toy_pool;
+/* loss_and_gradient (model.cpp:138-203) for `workers` ranks in one launch: rank w evaluates
+ * at params + (w / workers_per_row) * params_stride on the batch BatchStream::indices_for(step,
+ * w) selects through the device permutation `order` (dataset.cpp:141-151; world = workers);
+ * writes grad[w * grad_len ...] (FP32, the pad tail past param_count zeroed) and loss[w]
+ * (FP64).  FP64 arithmetic in the reference's operation order. */
+int dmb_toy_loss_grad(dmb_ctx* ctx, const dmb_toy_model* model, const dmb_toy_pool* pool,
+                      const int64_t* order, uint64_t step, uint64_t batch, const float* params,
+                      uint64_t params_stride, uint64_t workers_per_row, uint64_t workers,
+                      float* grad, uint64_t grad_len, double* loss, void* stream);
+/* forward_loss (model.cpp:127-136) over the whole pool at params: *loss (device FP64) */
+int dmb_toy_loss(dmb_ctx* ctx, const dmb_toy_model* model, const dmb_toy_pool* pool,
+                 const float* params, double* loss, void* stream);
+
 /* ---- status / counters ------------------------------------------------------- */
 /* synchronizes `stream`; DMB_TRAINING with *first_bad set if a non-finite gradient was
  * seen since the last call (the latch is then cleared), else DMB_OK */

@@ -43,6 +43,17 @@ class OptCfg(C.Structure):
     ]
 
 
+class ToyModel(C.Structure):
+    """dmb_toy_model (model.hpp:36-46)"""
+    _fields_ = [("kind", C.c_uint32), ("activation", C.c_uint32), ("loss", C.c_uint32), ("n_dims", C.c_uint32),
+                ("dims", C.c_uint32 * 9)]
+
+
+class ToyPool(C.Structure):
+    """dmb_toy_pool: a dataset split resident on the device"""
+    _fields_ = [("inputs", C.c_void_p), ("targets", C.c_void_p), ("labels", C.c_void_p), ("size", C.c_uint64)]
+
+
 class Update(C.Structure):
     _fields_ = [
         ("scheme", C.c_int32),
@@ -108,6 +119,8 @@ _SIGS = {
     "dmb_idct3": (C.c_int, [P, P, U64, U64, P, P]),
     "dmb_extract_fast_components": (C.c_int, [P, P, U64, U64, U64, P, P, P, P, P]),
     "dmb_sign_transform": (C.c_int, [P, P, U64, P]),
+    "dmb_toy_loss_grad": (C.c_int, [P, P, P, P, U64, U64, P, U64, U64, U64, P, U64, P, P]),
+    "dmb_toy_loss": (C.c_int, [P, P, P, P, P, P]),
     "dmb_latch_export": (C.c_int, [P, P, P]),
     "dmb_latch_import": (C.c_int, [P, P, P]),
     "dmb_kernel_timer_enable": (C.c_int, [C.c_int]),

@@ -50,7 +50,8 @@ import torch.distributed as dist
 
 from . import _capi
 from ._capi import lib
-from .core import (ConfigError, OptimizerConfig, OptimizerKind, ProtocolError, ReplicatorConfig, Scheme, TrainingError,
+from .core import (ConfigError, OptimizerConfig, OptimizerKind, ProtocolError, ReplicatorConfig, Scheme, StepTrace,
+                   TrainingError,
                    _check, _ptr, _stream, context, status)
 
 
@@ -300,7 +301,7 @@ class HybridCluster:
 
     def __init__(self, topo: Topology, param_count: int, opt: OptimizerConfig, rep: ReplicatorConfig,
                  initial_params: torch.Tensor, rank: int, shard_group=None, replica_group=None,
-                 buckets: int = 8, wire: str = "mask", exchange=None, world_group=None):
+                 buckets: int = 8, wire: str = "mask", exchange=None, world_group=None, trace: bool = False):
         self.topo, self.opt, self.rep = topo, opt, rep
         self.rank = rank
         self.node, self.accel = divmod(rank, topo.accels_per_node)
@@ -310,7 +311,12 @@ class HybridCluster:
         R, A = topo.nodes, topo.accels_per_node
         L = self.spec.real_len
         self.sgd = opt.kind == OptimizerKind.DemoSgd
-        self.fused = R == 1 and rep.scheme == Scheme.DeMo and L > 0  # one pass, double-buffered outputs
+        # R = 1 DeMo: one pass, double-buffered outputs; a traced step (StepTrace of every SGD
+        # prepare, optim.hpp:33-38) takes the prepare -> merge(R = 1) path instead
+        self.fused = R == 1 and rep.scheme == Scheme.DeMo and L > 0 and not trace
+        self._trace_bufs = (torch.empty(L, device=initial_params.device),
+                            torch.empty(L, device=initial_params.device)) if trace and opt.kind == OptimizerKind.DemoSgd \
+            else None
         self.params = initial_params[self.spec.offset:self.spec.offset + L].clone().contiguous()
         z = lambda: torch.zeros(L, dtype=torch.float32, device=self.device)  # noqa: E731
         if self.sgd:
@@ -390,8 +396,11 @@ class HybridCluster:
         return CollectiveExchange(shard_group, replica_group, world_group, R, A)
 
     # ---- phases -----------------------------------------------------------------
-    def begin(self, step: int, lr: float, grad_full: torch.Tensor) -> None:
-        """reduce-scatter, every bucket's prepare and the start of its exchange"""
+    def begin(self, step: int, lr: float, grad_full: torch.Tensor, trace=None) -> None:
+        """reduce-scatter, every bucket's prepare and the start of its exchange; `trace`
+        (SGD, a member built with trace=True) is called as trace(node, accel, StepTrace) with
+        the shard's m_accum, local_q and m_after (device views) after the prepares, as
+        run_step_hybrid's TraceSink (cluster.cpp:205-209)"""
         topo, L = self.topo, self.spec.real_len
         A, R = topo.accels_per_node, topo.nodes
         tr = StepTraffic(step=step, reduce_scatter_events=1, synchronize_events=1)
@@ -419,10 +428,13 @@ class HybridCluster:
                     lo, hi = b["lo"], b["hi"]
                     hdr = _capi.Update()
                     hdr.body = self.exchange.own(bi).data_ptr()
+                    tb = self._trace_bufs if trace is not None else None
                     if self.sgd:
                         _check(lib.dmb_demo_sgd_prepare(ctx, _ptr(self.g_shard[lo:hi]), _ptr(self.m[lo:hi]),
                                                         _ptr(self._m_next[lo:hi]), hi - lo, C.byref(o), C.byref(c),
-                                                        step, self.accel, C.byref(hdr), None, None, st))
+                                                        step, self.accel, C.byref(hdr),
+                                                        _ptr(tb[0][lo:hi]) if tb else None,
+                                                        _ptr(tb[1][lo:hi]) if tb else None, st))
                     else:
                         _check(lib.dmb_adamw_prepare(ctx, _ptr(self.g_shard[lo:hi]), hi - lo, C.byref(c), step,
                                                      self.accel, C.byref(hdr), None, st))
@@ -436,6 +448,11 @@ class HybridCluster:
                     self._pending.append((b, hdr, handle))
             finally:
                 lib.dmb_set_wire_format(ctx, 0)
+            if trace is not None:
+                if self._trace_bufs is None:
+                    raise ConfigError("a traced step needs a DemoSgd member built with trace=True")
+                trace(self.node, self.accel, StepTrace(m_accum=self._trace_bufs[1], local_q=self._trace_bufs[0],
+                                                       m_after=self._m_next))
         _check(lib.dmb_latch_export(ctx, _ptr(self.flag), st))
 
     def agree(self) -> None:

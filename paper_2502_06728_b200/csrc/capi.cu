@@ -1118,6 +1118,95 @@ int dmb_sign_transform(dmb_ctx* ctx, float* v, uint64_t n, void* stream) {
   return last_launch();
 }
 
+// ---- model.hpp toy producers (toy_models.cu) ---------------------------------------
+namespace {
+int toy_args(const dmb_toy_model* m, const dmb_toy_pool* pool, ToyArgs& a) {
+  if (!m || !pool) return fail(DMB_CONFIG, "model and pool are required");
+  if (m->kind > 1) return fail(DMB_CONFIG, "unknown model kind %u", m->kind);
+  if (m->n_dims == 0 || m->n_dims > (uint32_t)kToyMaxDims || (m->kind == 0 && m->n_dims != 1) ||
+      (m->kind == 1 && m->n_dims < 2))
+    return fail(DMB_CONFIG, "model dims: a quadratic model takes one, an mlp 2..%d", kToyMaxDims);
+  for (uint32_t l = 0; l < m->n_dims; ++l)
+    if (m->dims[l] == 0) return fail(DMB_CONFIG, "model dims must be positive");
+  if (m->kind == 1 && m->loss == 1 && !pool->labels)
+    return fail(DMB_CONFIG, "cross entropy batch is missing labels");  // model.cpp:24-27
+  if (m->kind == 1 && m->loss == 0 && !pool->targets)
+    return fail(DMB_CONFIG, "regression batch targets do not match model output dim");  // model.cpp:28-30
+  if (!pool->inputs || pool->size == 0) return fail(DMB_CONFIG, "empty batch");  // model.cpp:20
+  a = ToyArgs{};
+  a.kind = (int)m->kind;
+  a.activation = (int)m->activation;
+  a.loss_kind = (int)m->loss;
+  a.n_dims = m->n_dims;
+  for (uint32_t l = 0; l < m->n_dims; ++l) a.dims[l] = m->dims[l];
+  a.inputs = pool->inputs;
+  a.targets = pool->targets;
+  a.labels = pool->labels;
+  return DMB_OK;
+}
+uint64_t toy_param_count(const dmb_toy_model* m) {  // model.cpp:121-125
+  if (m->kind == 0) return m->dims[0];
+  uint64_t n = 0;
+  for (uint32_t l = 0; l + 1 < m->n_dims; ++l) n += (uint64_t)m->dims[l + 1] * m->dims[l] + m->dims[l + 1];
+  return n;
+}
+int toy_launch(const ToyArgs& a, cudaStream_t s) {
+  if (toy_smem_bytes(a) > 227 * 1024)
+    return fail(DMB_CONFIG, "toy producer: %llu B of shared memory (gradient + activations) exceed the 227 KB of an SM",
+                (unsigned long long)toy_smem_bytes(a));
+  launch_toy(a, s);
+  return last_launch();
+}
+}  // namespace
+
+int dmb_toy_loss_grad(dmb_ctx* ctx, const dmb_toy_model* model, const dmb_toy_pool* pool, const int64_t* order,
+                      uint64_t step, uint64_t batch, const float* params, uint64_t params_stride,
+                      uint64_t workers_per_row, uint64_t workers, float* grad, uint64_t grad_len, double* loss,
+                      void* stream) {
+  (void)ctx;
+  ToyArgs a;
+  if (int rc = toy_args(model, pool, a)) return rc;
+  if (batch == 0) return fail(DMB_CONFIG, "empty batch");
+  if (workers == 0 || workers_per_row == 0) return fail(DMB_CONFIG, "no workers");
+  if (workers * batch > pool->size)  // dataset.cpp:127-133
+    return fail(DMB_CONFIG, "global batch %llu x %llu exceeds the training pool of %llu examples",
+                (unsigned long long)workers, (unsigned long long)batch, (unsigned long long)pool->size);
+  if (grad_len < toy_param_count(model) || params_stride < toy_param_count(model))
+    return fail(DMB_CONFIG, "parameter vector too short: %llu < %llu", (unsigned long long)params_stride,
+                (unsigned long long)toy_param_count(model));  // model.cpp:15-19
+  if (!order) return fail(DMB_CONFIG, "the batch permutation is required");
+  a.order = order;
+  a.order_len = pool->size;
+  a.step = step;
+  a.world = workers;
+  a.batch = batch;
+  a.params = params;
+  a.params_stride = params_stride;
+  a.workers_per_row = workers_per_row;
+  a.workers = workers;
+  a.grad = grad;
+  a.grad_stride = grad_len;
+  a.grad_len = grad_len;
+  a.loss = loss;
+  return toy_launch(a, as_stream(stream));
+}
+
+int dmb_toy_loss(dmb_ctx* ctx, const dmb_toy_model* model, const dmb_toy_pool* pool, const float* params,
+                 double* loss, void* stream) {
+  (void)ctx;
+  ToyArgs a;
+  if (int rc = toy_args(model, pool, a)) return rc;
+  a.order = nullptr;
+  a.batch = pool->size;
+  a.world = 1;
+  a.params = params;
+  a.params_stride = toy_param_count(model);
+  a.workers_per_row = 1;
+  a.workers = 1;
+  a.loss = loss;
+  return toy_launch(a, as_stream(stream));
+}
+
 int dmb_extract_fast_components(dmb_ctx* ctx, const float* v, uint64_t len, uint64_t chunk_size, uint64_t top_k,
                                 uint32_t* indices, float* coeffs, float* fast, float* residual, void* stream) {
   cudaStream_t s = as_stream(stream);

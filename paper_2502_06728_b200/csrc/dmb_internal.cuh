@@ -231,6 +231,29 @@ void launch_dct(bool inverse, const float* in, uint64_t n, uint64_t count, const
 void launch_sign(float* v, uint64_t n, cudaStream_t st);
 void launch_residual(const float* v, const float* fast, uint64_t n, bool full_band, float* res, cudaStream_t st);
 
+// toy gradient producers (toy_models.cu; model.cpp) for the trainer loop
+constexpr int kToyMaxDims = 9;  // an input and up to 8 layers
+struct ToyArgs {
+  int kind;           // 0 quadratic, 1 mlp
+  int activation;     // 0 tanh, 1 relu
+  int loss_kind;      // 0 mse, 1 cross entropy
+  uint32_t n_dims;
+  uint32_t dims[kToyMaxDims];
+  const double* inputs;    // pool x dims[0]
+  const double* targets;   // pool x dims.back() (mse) or null
+  const int32_t* labels;   // pool (cross entropy) or null
+  const int64_t* order;    // BatchStream permutation, or null: examples 0..batch-1
+  uint64_t order_len;
+  uint64_t step, world, batch;
+  const float* params;     // rows of params_stride; worker w reads row w / workers_per_row
+  uint64_t params_stride, workers_per_row, workers;
+  float* grad;             // workers x grad_stride, grad_len written (pad zeroed); null: loss only
+  uint64_t grad_stride, grad_len;
+  double* loss;            // workers
+};
+uint64_t toy_smem_bytes(const ToyArgs& a);
+int launch_toy(const ToyArgs& a, cudaStream_t stream);
+
 // Random index sets (replicate.cpp:160-172) on the device.
 struct RandomScratch {
   uint32_t* draws;   // j_i for the L - count iterations that decide the set
