@@ -12,10 +12,10 @@
 //   apply warps 8-11  (slice layout, tcgen05.ld 32x32b: thread = chunk row)
 //        - D = IDCT(W) and the raw gradient from TMEM, p / exp_avg / exp_avg_sq from the
 //          shared-memory staging tile (TMA), decoupled AdamW (or SGD) in place there
-//        - then the front of tile t+2: gradient tile (TMA, 128B swizzle) -> TF32 hi/lo +
-//          raw copy -> TMEM, ||x||_1 per chunk, require_finite
-//   MMA warp 12       - gradient TMA and every tcgen05.mma, in tile order: forward
-//                       C = X B^T and inverse D = W B in 3xTF32 (A from TMEM)
+//        - then the front of tile t+2: gradient tile (TMA issued by these warps, 128B
+//          swizzle) -> TF32 hi/lo + raw copy -> TMEM, ||x||_1 per chunk, require_finite
+//   MMA warp 12       - every tcgen05.mma, in tile order: forward C = X B^T and inverse
+//                       D = W B in 3xTF32 (A from TMEM)
 //   state warp 13     - optimizer-state TMA loads / stores (two 32-column halves)
 // The optimizer state streams through shared memory with TMA bulk tensor copies, so the
 // HBM traffic of tile t overlaps the selection of tile t+1 without occupying registers.
@@ -57,7 +57,7 @@ constexpr int S = 64;
 constexpr int TM = 128;
 constexpr int kSelWarps = 8;
 constexpr int kAppWarps = 4;
-constexpr int kMmaWarp = kSelWarps + kAppWarps;  // gradient TMA + every tcgen05.mma
+constexpr int kMmaWarp = kSelWarps + kAppWarps;  // every tcgen05.mma
 constexpr int kMemWarp = kMmaWarp + 1;           // optimizer-state TMA loads / stores
 constexpr int THREADS = (kMemWarp + 1) * 32;
 
@@ -75,11 +75,15 @@ constexpr uint32_t OFF_G = 4 * BMAT;            // gradient tile (TMA, swizzled)
 constexpr uint32_t OFF_ST = OFF_G + TILE;       // p, exp_avg, exp_avg_sq staging tiles
 constexpr uint32_t OFF_SCR = OFF_ST + 3 * TILE; // merge grids (8 x 4 KB)
 constexpr uint32_t SCR_WARP = 4096;
+constexpr uint32_t kRingWarpSgd = 12288;  // MergeSgd ring per select warp (staging tiles 1-2 + scratch)
+constexpr int kRingMax = 16;  // cp.async groups the ring keeps in flight at most
 constexpr int kStageMax = 10;  // MASK_SIGN members staged per warp: 16 rows x (16 + 8) B each in SCR_WARP
 constexpr uint32_t OFF_BAR = OFF_SCR + kSelWarps * SCR_WARP;
 constexpr uint32_t OFF_L1 = OFF_BAR + 256;      // ||x||_1 per chunk, two tiles
 constexpr uint32_t SMEM_BYTES = OFF_L1 + 2 * TM * 4;
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+static_assert(kSelWarps * kRingWarpSgd == 2 * TILE + kSelWarps * SCR_WARP && OFF_SCR == OFF_ST + 3 * TILE,
+              "the MergeSgd ring covers staging tiles 1-2 and the scratch exactly");
 
 constexpr uint32_t COL_C = 0, COL_D = 64, COL_XH = 128, COL_XL = 192, COL_G = 256;
 // SGD modes: W1 = coef on the selection (X columns) and D1 = IDCT(W1) = local_q; the front
@@ -128,6 +132,21 @@ __device__ __forceinline__ void tma_2d_store(const CUtensorMap* map, int c0, int
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// cp.async.wait_group with a run-time count (warp-uniform, 0..kRingMax-1)
+__device__ __forceinline__ void cp_async_wait_pending(int n) {
+  switch (n) {
+#define DMB_WAIT_CASE(N) \
+  case N:                \
+    asm volatile("cp.async.wait_group " #N ";" ::: "memory"); \
+    break;
+    DMB_WAIT_CASE(0) DMB_WAIT_CASE(1) DMB_WAIT_CASE(2) DMB_WAIT_CASE(3) DMB_WAIT_CASE(4) DMB_WAIT_CASE(5)
+    DMB_WAIT_CASE(6) DMB_WAIT_CASE(7) DMB_WAIT_CASE(8) DMB_WAIT_CASE(9) DMB_WAIT_CASE(10) DMB_WAIT_CASE(11)
+    DMB_WAIT_CASE(12) DMB_WAIT_CASE(13) DMB_WAIT_CASE(14)
+#undef DMB_WAIT_CASE
+    default:
+      asm volatile("cp.async.wait_group 15;" ::: "memory");
+  }
+}
 
 // 16 TMEM lanes x 64 columns: thread t gets lanes base + t/4 (regs 4r, 4r+1) and
 // base + 8 + t/4 (regs 4r+2, 4r+3) at columns 8r + 2(t%4) + {0, 1}
@@ -219,10 +238,35 @@ __device__ __forceinline__ uint64_t spread(uint32_t bits, int s) {
   return m;
 }
 __device__ __forceinline__ uint32_t gather16(uint64_t m, int s) {  // inverse of spread
-  uint32_t b = 0;
-#pragma unroll
-  for (int r = 0; r < 8; ++r) b |= (uint32_t)((m >> (8 * r + 2 * s)) & 3u) << (2 * r);
-  return b;
+  // bits 8r + 2s + b -> 2r + b: pairs to the bottom of their bytes, then compress
+  uint64_t t = (m >> (2 * s)) & 0x0303030303030303ull;
+  t = (t | (t >> 6)) & 0x000F000F000F000Full;
+  t = (t | (t >> 12)) & 0x000000FF000000FFull;
+  return (uint32_t)(t | (t >> 24)) & 0xffffu;
+}
+// value ranks in a chunk's frequency mask m (values stored in ascending frequency): byte r of
+// the result is the number of selected columns below column 8r + 2s -- those of the bytes before
+// r (SWAR popcount per byte, prefix by multiplication) plus those of byte r below the pair
+__device__ __forceinline__ uint64_t byte_popc(uint64_t x) {
+  x = x - ((x >> 1) & 0x5555555555555555ull);
+  x = (x & 0x3333333333333333ull) + ((x >> 2) & 0x3333333333333333ull);
+  return (x + (x >> 4)) & 0x0f0f0f0f0f0f0f0full;
+}
+__device__ __forceinline__ uint64_t pair_ranks(uint64_t m, int s) {
+  const uint64_t x = byte_popc(m);
+  const uint64_t excl = x * 0x0101010101010101ull - x;  // bytes <= 64: no carries
+  return excl + byte_popc(m & (((1ull << (2 * s)) - 1ull) * 0x0101010101010101ull));
+}
+__device__ __forceinline__ float lds_wire(const uint8_t* p, uint32_t t, int vd) {  // fp32 / fp16 in shared memory
+  const uint32_t a = smem_u32(p);
+  if (vd == DMB_FP32) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a + 4 * t));
+    return v;
+  }
+  unsigned short h;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a + 2 * t));
+  return __half2float(__ushort_as_half(h));
 }
 
 __device__ __forceinline__ int count_ge16(const float (&c)[16], float t) {
@@ -977,6 +1021,53 @@ __global__ void __maxnreg__(128)
     // MASK_SIGN merges: the warp's 16 rows of every member (16 B of codes + the 8 B mask per
     // row) into the scratch with cp.async; committed, waited for by the decode
     bool prefetched = false;
+    // MASK merges with values (fp32, fp16 at even k): every (tile, member) pair of this warp's
+    // stream -- its 16 rows' masks (128 B) then their values (16 k vb B) -- is copied with
+    // cp.async into a ring of ring_slots slots, ring_slots - 1 pairs ahead of the decode and
+    // across tile boundaries, so the R dependent mask -> value round trips of a tile become one
+    // pipelined stream.  MergeSgd has no gradient and only the p staging tile: its ring takes
+    // the free staging tiles 1-2 and the scratch (12 KB per warp); MergeAdam the scratch (4 KB).
+    const int mvd = kMerge ? mask_value_dtype(a.geo) : DMB_TERNARY;
+    const uint32_t mvb = mvd == DMB_FP32 ? 4u : 2u;
+    uint8_t* const ring = kMergeSgd ? smem + OFF_ST + TILE + warp * kRingWarpSgd : scr;
+    const uint32_t ring_sb = 128u + ((16u * (uint32_t)k * mvb + 15u) & ~15u);
+    const int ring_slots = (!kMerge || !a.geo.wire_mask || mvd == DMB_TERNARY || (mvd == DMB_FP16 && (k & 1)))
+                               ? 0
+                               : (int)min((kMergeSgd ? kRingWarpSgd : SCR_WARP) / ring_sb, (uint32_t)kRingMax);
+    uint64_t ring_next = 0;  // next pair to issue
+    auto ring_issue = [&](uint64_t p) {
+      const int R = a.in.R;
+      const uint64_t pt = blockIdx.x + (p / (uint64_t)R) * G;
+      const int rr = (int)(p % (uint64_t)R);
+      uint8_t* slot = ring + (uint32_t)(p % (uint64_t)ring_slots) * ring_sb;
+      if (pt < ntiles) {
+        const uint64_t wrow = pt * TM + base;
+        const int nrows = wrow < nfull ? (nfull - wrow < 16 ? (int)(nfull - wrow) : 16) : 0;
+        const uint8_t* body = a.in.body[rr];
+        if (lane < nrows)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(slot + 8 * lane)),
+                       "l"(body + (wrow + lane) * 8)
+                       : "memory");
+        // values: 4-byte aligned (fp32, or fp16 at even k), 8-byte pieces and a 4-byte tail
+        const uint8_t* src = body + nchunks * 8 + wrow * (uint64_t)k * mvb;
+        const uint32_t bytes = (uint32_t)nrows * (uint32_t)k * mvb;
+        const bool a8 = ((reinterpret_cast<uintptr_t>(src)) & 7u) == 0;
+        if (a8) {
+          for (uint32_t o = 8 * lane; o + 8 <= bytes; o += 256)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(slot + 128 + o)), "l"(src + o)
+                         : "memory");
+          if ((bytes & 7u) && lane == 0)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot + 128 + (bytes & ~7u))),
+                         "l"(src + (bytes & ~7u))
+                         : "memory");
+        } else {
+          for (uint32_t o = 4 * lane; o + 4 <= bytes; o += 128)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(slot + 128 + o)), "l"(src + o)
+                         : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");  // one group per pair, empty or not
+    };
     auto stage_rows = [&](uint64_t* stg, uint64_t wrow) {
       const int R = a.in.R;
       for (int pr = lane; pr < R * 16; pr += 32) {
@@ -1245,6 +1336,41 @@ __global__ void __maxnreg__(128)
             }
             sel0 = act0 ? gather16(om0, s) : 0u;
             sel1 = act1 ? gather16(om1, s) : 0u;
+          } else if (ring_slots > 0) {
+          // MASK bodies with values: member by member from the ring (ring_issue), in member order
+          uint64_t om0 = 0, om1 = 0;
+          const int q0 = lane >> 2;
+          const int R = a.in.R;
+          for (int rr = 0; rr < R; ++rr) {
+            const uint64_t pr = (uint64_t)it * (uint64_t)R + (uint64_t)rr;
+            while (ring_next < pr + (uint64_t)ring_slots) ring_issue(ring_next++);
+            cp_async_wait_pending(ring_slots - 1);  // the group of pair pr has landed
+            __syncwarp();
+            const uint8_t* slot = ring + (uint32_t)(pr % (uint64_t)ring_slots) * ring_sb;
+            const uint64_t* smk = reinterpret_cast<const uint64_t*>(slot);
+            const uint8_t* sv = slot + 128;
+            const uint64_t m0 = act0 ? smk[q0] : 0ull, m1 = act1 ? smk[q0 + 8] : 0ull;
+            if (s == 0 && ((act0 && __popcll(m0) != k) || (act1 && __popcll(m1) != k)))
+              atomicExch(&a.status->protocol_error, 1u);
+            // the value of column 8r + 2s + b is number rank_r + b * (bit of 8r + 2s) of the row
+            const uint64_t rk0 = pair_ranks(m0, s), rk1 = pair_ranks(m1, s);
+            const uint32_t tb0 = gather16(m0, s), tb1 = gather16(m1, s);  // bit e: column qcol(e, s)
+            const uint32_t o0 = (uint32_t)q0 * k, o1 = (uint32_t)(q0 + 8) * k;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const uint32_t n0 = (uint32_t)(rk0 >> (8 * (e >> 1))) & 0xffu, n1 = (uint32_t)(rk1 >> (8 * (e >> 1))) & 0xffu;
+              const uint32_t x0 = (e & 1) ? (tb0 >> (e - 1)) & 1u : 0u, x1 = (e & 1) ? (tb1 >> (e - 1)) & 1u : 0u;
+              if ((tb0 >> e) & 1u) gq0[e] += lds_wire(sv, o0 + n0 + x0, vd);
+              if ((tb1 >> e) & 1u) gq1[e] += lds_wire(sv, o1 + n1 + x1, vd);
+            }
+            if (rr == a.own_rank) {
+              om0 = m0;
+              om1 = m1;
+            }
+            __syncwarp();  // the slot may be refilled
+          }
+          sel0 = act0 ? gather16(om0, s) : 0u;
+          sel1 = act1 ? gather16(om1, s) : 0u;
           } else {
           uint64_t om0 = 0, om1 = 0;
           auto fetch = [&](int rr, uint64_t& m0, uint64_t& m1) {

@@ -139,11 +139,12 @@ def test_04a_single_worker_full_equals_baseline_loop(T, gold):
     assert gap <= TRAJ_TOL, gap
 
 
-def _lockstep_gap(T, text_a, text_b, same_world=True):
+def _lockstep_gap(T, text_a, text_b):
     ta, tb = T.Trainer(T.parse_config(text_a)), T.Trainer(T.parse_config(text_b))
     worst = 0.0
     for step in range(ta.cfg.steps):
-        ma, mb = ta.run_step(step), tb.run_step(step)
+        ta.run_step(step)
+        tb.run_step(step)
         for node in range(min(ta.cfg.nodes, tb.cfg.nodes)):
             worst = max(worst, float((ta.worker_params(node) - tb.worker_params(node)).abs().max()))
     return ta, tb, worst

@@ -43,6 +43,7 @@ def main():
     ap.add_argument("--tiles-per-cta", type=int, default=40)
     ap.add_argument("--k", type=int, default=32)
     ap.add_argument("--R", type=int, default=4)
+    ap.add_argument("--sign", type=int, default=1, help="1: sign-mode payloads (MASK_SIGN), 0: fp32 values (MASK)")
     a = ap.parse_args()
     lib = _capi.lib
     lib.dmb_debug_events.argtypes = [C.c_void_p]
@@ -51,7 +52,7 @@ def main():
     L = sms * a.tiles_per_cta * 8192
     ctx = context(0).h
     sp = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-    cfg = P.ReplicatorConfig(P.Scheme.DeMo, 64, a.k, a.k / 64, True, P.TransferDtype.Fp32, 1234)
+    cfg = P.ReplicatorConfig(P.Scheme.DeMo, 64, a.k, a.k / 64, bool(a.sign), P.TransferDtype.Fp32, 1234)
     c = cfg.c()
     o_adam = P.OptimizerConfig(P.OptimizerKind.DecoupledAdamW).c()
     o_sgd = P.OptimizerConfig(P.OptimizerKind.DemoSgd, momentum_decay=0.9).c()
@@ -124,7 +125,7 @@ def main():
     t = ev[: 32 * 32].reshape(32, 32)
     base = t[0, 0]
     ids = [i for i in (2, 3, 18, 19, 0, 1, 4, 5, 6, 7, 8, 9, 14, 15, 10, 11, 12, 13, 16, 17) if t[:, i].any()]
-    print(f"mode {a.mode}: L = {L} ({a.tiles_per_cta} tiles per CTA), step {e0.elapsed_time(e1):.3f} ms, "
+    print(f"mode {a.mode} (k {a.k}, sign {a.sign}, R {a.R}): L = {L} ({a.tiles_per_cta} tiles per CTA), step {e0.elapsed_time(e1):.3f} ms, "
           f"{e0.elapsed_time(e1) * 1e3 / a.tiles_per_cta:.2f} us per tile per CTA")
     print("tile " + " ".join(f"{NAMES[i]:>10s}" for i in ids) + "   period")
     for it in range(32):

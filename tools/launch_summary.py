@@ -9,7 +9,7 @@ import sys
 def main(path):
     hdr = None
     agg = collections.defaultdict(lambda: [0, 0.0])
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
     with open(path) as f:
         for r in csv.reader(f):
             if len(r) > 5 and r[0] == "ID":

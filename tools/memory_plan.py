@@ -7,7 +7,8 @@ Counted (the allocation rules of cluster.py, FP32 state):
   R = 1 (fused step): the double-buffered outputs (p, and the moments for AdamW);
   the caller's full padded gradient and, with A > 1, the reduce-scattered shard;
   the exchange: own bucket slots x 2 (symmetric memory, alternating by step) + the R gathered
-  copies (all buckets resident: the step encodes every bucket before the refusal agreement).
+  copies (all buckets resident: the step encodes every bucket before the refusal agreement);
+  "windowed": the same with the exchange bounded by the budget of the memory-bounded windows.
 Bodies: MASK_SIGN 24 B per 64-chunk (sign / ternary), MASK 8 + k * bits / 8 B per chunk,
 reference body k * (4 + bits / 8) B per chunk (include/demo_b200.h).
 
@@ -39,9 +40,12 @@ def plan(model, S, R, opt, k=32, sign=True, wire="mask"):
     b = body_bytes(L, k, sign, wire=wire) if R > 1 else 0
     ex = b * (2 + R) if R > 1 else 0
     total = st + grads + ex
+    # above the budget (a quarter of the device) HybridCluster runs the buckets in windows whose
+    # slots fit it (cluster.py, DMB_GATHER_BUDGET)
+    windowed = st + grads + min(ex, 0.25 * HBM)
     return dict(model=model, layout=f"{S}x{R}", optimizer=opt, k=k, sign=sign, wire=wire,
                 state_gb=st / GB, gradients_gb=grads / GB, exchange_gb=ex / GB, total_gb=total / GB,
-                fits=total < HBM)
+                windowed_gb=windowed / GB, fits=windowed < HBM)
 
 
 def main():
@@ -53,10 +57,10 @@ def main():
         rows.append(plan("OLMo-2-1B", S, R, "adamw"))
     rows.append(plan("T5-base", 4, 2, "sgd"))
     print(f"{'model':10s} {'layout':6s} {'opt':6s} {'k':>3s} {'sign':5s} {'state':>7s} {'grads':>7s} "
-          f"{'exchange':>8s} {'total GB':>9s}  fits 180 GB")
+          f"{'exchange':>8s} {'total GB':>9s} {'windowed':>9s}  fits 180 GB")
     for r in rows:
         print(f"{r['model']:10s} {r['layout']:6s} {r['optimizer']:6s} {r['k']:3d} {str(r['sign']):5s} "
-              f"{r['state_gb']:7.1f} {r['gradients_gb']:7.1f} {r['exchange_gb']:8.1f} {r['total_gb']:9.1f}  "
+              f"{r['state_gb']:7.1f} {r['gradients_gb']:7.1f} {r['exchange_gb']:8.1f} {r['total_gb']:9.1f} {r['windowed_gb']:9.1f}  "
               f"{'yes' if r['fits'] else 'NO'}")
 
 
