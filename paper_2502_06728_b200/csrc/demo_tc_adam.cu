@@ -82,8 +82,9 @@ constexpr uint32_t OFF_BAR = OFF_SCR + kSelWarps * SCR_WARP;
 constexpr uint32_t OFF_L1 = OFF_BAR + 256;      // ||x||_1 per chunk, two tiles
 constexpr uint32_t SMEM_BYTES = OFF_L1 + 2 * TM * 4;
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
-static_assert(kSelWarps * kRingWarpSgd == 2 * TILE + kSelWarps * SCR_WARP && OFF_SCR == OFF_ST + 3 * TILE,
-              "the MergeSgd ring covers staging tiles 1-2 and the scratch exactly");
+static_assert(kSelWarps * kRingWarpSgd == 2 * TILE + kSelWarps * SCR_WARP && OFF_SCR == OFF_ST + 3 * TILE &&
+                  kSelWarps * 4096 == 2 * BMAT && kSelWarps * 4096 == TILE,
+              "the MergeSgd ring covers the forward basis, the gradient stage, staging tiles 1-2 and the scratch");
 
 constexpr uint32_t COL_C = 0, COL_D = 64, COL_XH = 128, COL_XL = 192, COL_G = 256;
 // SGD modes: W1 = coef on the selection (X columns) and D1 = IDCT(W1) = local_q; the front
@@ -256,17 +257,6 @@ __device__ __forceinline__ uint64_t pair_ranks(uint64_t m, int s) {
   const uint64_t x = byte_popc(m);
   const uint64_t excl = x * 0x0101010101010101ull - x;  // bytes <= 64: no carries
   return excl + byte_popc(m & (((1ull << (2 * s)) - 1ull) * 0x0101010101010101ull));
-}
-__device__ __forceinline__ float lds_wire(const uint8_t* p, uint32_t t, int vd) {  // fp32 / fp16 in shared memory
-  const uint32_t a = smem_u32(p);
-  if (vd == DMB_FP32) {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a + 4 * t));
-    return v;
-  }
-  unsigned short h;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a + 2 * t));
-  return __half2float(__ushort_as_half(h));
 }
 
 __device__ __forceinline__ int count_ge16(const float (&c)[16], float t) {
@@ -1025,21 +1015,38 @@ __global__ void __maxnreg__(128)
     // stream -- its 16 rows' masks (128 B) then their values (16 k vb B) -- is copied with
     // cp.async into a ring of ring_slots slots, ring_slots - 1 pairs ahead of the decode and
     // across tile boundaries, so the R dependent mask -> value round trips of a tile become one
-    // pipelined stream.  MergeSgd has no gradient and only the p staging tile: its ring takes
-    // the free staging tiles 1-2 and the scratch (12 KB per warp); MergeAdam the scratch (4 KB).
+    // pipelined stream.  MergeSgd has no gradient, no forward DCT and only the p staging tile: its
+    // ring takes the forward basis, the gradient stage, the staging tiles 1-2 and the scratch
+    // (20 KB per warp); MergeAdam the scratch (4 KB).
     const int mvd = kMerge ? mask_value_dtype(a.geo) : DMB_TERNARY;
     const uint32_t mvb = mvd == DMB_FP32 ? 4u : 2u;
+    // MergeSgd also takes the forward basis (no forward DCT) and the gradient stage (no gradient):
+    // slots in three pieces per warp, 4 + 4 + 12 KB
+    // (16 spare bytes: an unselected column's rank may run one value past the last row)
+    const uint32_t ring_sb = 128u + ((16u * (uint32_t)k * mvb + 15u) & ~15u) + 16u;
+    const bool ring_on = kMerge && a.geo.wire_mask && mvd != DMB_TERNARY && !(mvd == DMB_FP16 && (k & 1));
+    const uint32_t nA = kMergeSgd ? 4096u / ring_sb : 0u, nB = nA;
+    uint8_t* const ringA = smem + OFF_BHI + warp * 4096;
+    uint8_t* const ringB = smem + OFF_G + warp * 4096;
     uint8_t* const ring = kMergeSgd ? smem + OFF_ST + TILE + warp * kRingWarpSgd : scr;
-    const uint32_t ring_sb = 128u + ((16u * (uint32_t)k * mvb + 15u) & ~15u);
-    const int ring_slots = (!kMerge || !a.geo.wire_mask || mvd == DMB_TERNARY || (mvd == DMB_FP16 && (k & 1)))
-                               ? 0
-                               : (int)min((kMergeSgd ? kRingWarpSgd : SCR_WARP) / ring_sb, (uint32_t)kRingMax);
-    uint64_t ring_next = 0;  // next pair to issue
-    auto ring_issue = [&](uint64_t p) {
-      const int R = a.in.R;
-      const uint64_t pt = blockIdx.x + (p / (uint64_t)R) * G;
-      const int rr = (int)(p % (uint64_t)R);
-      uint8_t* slot = ring + (uint32_t)(p % (uint64_t)ring_slots) * ring_sb;
+    const int ring_slots =
+        ring_on ? (int)min(nA + nB + (kMergeSgd ? kRingWarpSgd : SCR_WARP) / ring_sb, (uint32_t)kRingMax) : 0;
+    auto ring_slot = [&](uint32_t i) -> uint8_t* {
+      return i < nA ? ringA + i * ring_sb : (i < nA + nB ? ringB + (i - nA) * ring_sb : ring + (i - nA - nB) * ring_sb);
+    };
+    // the next pair to issue: its tile, member and slot; pairs issued and not yet decoded
+    uint64_t iss_tile = tile;
+    int iss_rr = 0, iss_slot = 0, ring_ahead = 0, con_slot = 0;
+    auto ring_issue = [&]() {
+      const uint64_t pt = iss_tile;
+      const int rr = iss_rr;
+      uint8_t* slot = ring_slot((uint32_t)iss_slot);
+      iss_slot = iss_slot + 1 == ring_slots ? 0 : iss_slot + 1;
+      if (++iss_rr == a.in.R) {
+        iss_rr = 0;
+        iss_tile += G;
+      }
+      ++ring_ahead;
       if (pt < ntiles) {
         const uint64_t wrow = pt * TM + base;
         const int nrows = wrow < nfull ? (nfull - wrow < 16 ? (int)(nfull - wrow) : 16) : 0;
@@ -1342,11 +1349,12 @@ __global__ void __maxnreg__(128)
           const int q0 = lane >> 2;
           const int R = a.in.R;
           for (int rr = 0; rr < R; ++rr) {
-            const uint64_t pr = (uint64_t)it * (uint64_t)R + (uint64_t)rr;
-            while (ring_next < pr + (uint64_t)ring_slots) ring_issue(ring_next++);
-            cp_async_wait_pending(ring_slots - 1);  // the group of pair pr has landed
+            while (ring_ahead < ring_slots) ring_issue();  // this pair and ring_slots - 1 more in flight
+            cp_async_wait_pending(ring_slots - 1);  // the group of this pair has landed
             __syncwarp();
-            const uint8_t* slot = ring + (uint32_t)(pr % (uint64_t)ring_slots) * ring_sb;
+            const uint8_t* slot = ring_slot((uint32_t)con_slot);
+            con_slot = con_slot + 1 == ring_slots ? 0 : con_slot + 1;
+            --ring_ahead;
             const uint64_t* smk = reinterpret_cast<const uint64_t*>(slot);
             const uint8_t* sv = slot + 128;
             const uint64_t m0 = act0 ? smk[q0] : 0ull, m1 = act1 ? smk[q0 + 8] : 0ull;
@@ -1356,12 +1364,29 @@ __global__ void __maxnreg__(128)
             const uint64_t rk0 = pair_ranks(m0, s), rk1 = pair_ranks(m1, s);
             const uint32_t tb0 = gather16(m0, s), tb1 = gather16(m1, s);  // bit e: column qcol(e, s)
             const uint32_t o0 = (uint32_t)q0 * k, o1 = (uint32_t)(q0 + 8) * k;
+            // branch-free: every column loads (an unselected one at most one value past the
+            // rows, inside the slot's padding) and a select keeps the unselected entries as they
+            // are (bit-identical to adding only the selected ones)
+            auto add_row = [&](float (&gq)[16], uint32_t tb, uint64_t rk, uint32_t o, auto ld) {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const uint32_t n0 = (uint32_t)(rk0 >> (8 * (e >> 1))) & 0xffu, n1 = (uint32_t)(rk1 >> (8 * (e >> 1))) & 0xffu;
-              const uint32_t x0 = (e & 1) ? (tb0 >> (e - 1)) & 1u : 0u, x1 = (e & 1) ? (tb1 >> (e - 1)) & 1u : 0u;
-              if ((tb0 >> e) & 1u) gq0[e] += lds_wire(sv, o0 + n0 + x0, vd);
-              if ((tb1 >> e) & 1u) gq1[e] += lds_wire(sv, o1 + n1 + x1, vd);
+              for (int r = 0; r < 8; ++r) {
+                const uint32_t n = o + ((uint32_t)(rk >> (8 * r)) & 0xffu);
+                const uint32_t b0 = (tb >> (2 * r)) & 1u, b1 = (tb >> (2 * r + 1)) & 1u;
+                const float v0 = ld(n), v1 = ld(n + b0);
+                gq[2 * r] = b0 ? gq[2 * r] + v0 : gq[2 * r];
+                gq[2 * r + 1] = b1 ? gq[2 * r + 1] + v1 : gq[2 * r + 1];
+              }
+            };
+            if (vd == DMB_FP32) {
+              const float* f = reinterpret_cast<const float*>(sv);
+              auto ld = [&](uint32_t t) { return f[t]; };
+              add_row(gq0, tb0, rk0, o0, ld);
+              add_row(gq1, tb1, rk1, o1, ld);
+            } else {
+              const __half* h = reinterpret_cast<const __half*>(sv);
+              auto ld = [&](uint32_t t) { return __half2float(h[t]); };
+              add_row(gq0, tb0, rk0, o0, ld);
+              add_row(gq1, tb1, rk1, o1, ld);
             }
             if (rr == a.own_rank) {
               om0 = m0;
