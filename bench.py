@@ -57,6 +57,9 @@ def parse():
                     help="N>1: SMs the step kernels leave free for the concurrent NCCL all-gather")
     ap.add_argument("--cpu-sample", type=int, default=1 << 22, help="elements per CPU thread")
     ap.add_argument("--layout", default=None, help="SxR (shards x replicas) for N>1; default 1xN")
+    ap.add_argument("--pull-rs", type=int, default=1,
+                    help="S>1: the gradients live in symmetric memory and every rank pulls its shard over NVLink "
+                         "bucket by bucket under the step kernels (0: NCCL reduce-scatter)")
     ap.add_argument("--grad-ring", type=int, default=3, help="pre-generated gradients, one per step in turn")
     return ap.parse_args()
 
@@ -277,8 +280,12 @@ def run_ours(args, rank, world, local_rank):
         topo = Topology(nodes=R, accels_per_node=S)
         sg, rg = groups_for(topo, rank)
         os.environ["DMB_SM_RESERVE"] = str(args.sm_reserve)
-        cluster = HybridCluster(topo, L, opt, cfg, params, rank, sg, rg, buckets=args.buckets, wire=args.wire)
+        cluster = HybridCluster(topo, L, opt, cfg, params, rank, sg, rg, buckets=args.buckets, wire=args.wire,
+                                pull_grads=bool(args.pull_rs) and S > 1)
         del params
+        if cluster.pull:  # the ring is the two symmetric gradient buffers, alternating by step
+            grads = [cluster.grad_buffer(i).normal_(0.0, 1e-3, generator=gen) for i in range(2)]
+            grad = grads[0]
 
     def check(rc):
         if rc != 0:
@@ -381,8 +388,9 @@ def run_ours(args, rank, world, local_rank):
         t0 = time.perf_counter()
         ev2[0].record(stream)
         for k in range(e_steps):
-            grad.copy_(host_g, non_blocking=True)  # H2D of the step's input
-            step_once(100 + k, grad)
+            g_in = cluster.grad_buffer(100 + k) if distributed and cluster.pull else grad
+            g_in[:L].copy_(host_g, non_blocking=True)  # H2D of the step's input
+            step_once(100 + k, g_in)
             check(lib.dmb_status(ctx, sp, C.byref(status_h)))  # D2H of the step result (status word)
         ev2[1].record(stream)
         torch.cuda.synchronize()
@@ -423,7 +431,13 @@ def run_ours(args, rank, world, local_rank):
             "metric": METRIC, "value": value, "unit": "params/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (N(0,1e-3^2) gradients, N(0,0.02^2) params)",
-            "config": dict(config_dict(args, world, args.layout), gradients=f"ring of {args.grad_ring} synthetic gradients, the next one every step"),
+            "config": dict(config_dict(args, world, args.layout),
+                           gradients=(f"ring of {args.grad_ring} synthetic gradients, the next one every step"
+                                      if not (distributed and cluster.pull) else
+                                      "two synthetic gradients in symmetric memory, alternating by step"),
+                           **({"reduce_scatter": "pulled over NVLink under the step kernels" if cluster.pull
+                               else "NCCL reduce_scatter(AVG)"} if distributed and cluster.topo.accels_per_node > 1
+                              else {})),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "kernel": ("demo_tc_adam_kernel<StepAdam> (tcgen05, warp-specialised)"

@@ -224,6 +224,13 @@ int dmb_step_adamw_local(dmb_ctx* ctx, const float* grad, const float* p_in, flo
 int dmb_grad_mean(dmb_ctx* ctx, const float* const* grads, uint64_t members, uint64_t len,
                   float* out, void* stream);
 
+/* the same mean pulled over NVLink: `grads` may point into the shard-group peers' memory mapped
+ * into this device (symmetric memory); a persistent grid of at most `ctas` CTAs (0: one wave over
+ * every SM) with 16-byte loads in flight, so it can run beside a step kernel that leaves those
+ * SMs free (DMB_SM_RESERVE) -- the reduce-scatter of bucket b+1 under the prepare of bucket b */
+int dmb_grad_mean_pull(dmb_ctx* ctx, const float* const* grads, uint64_t members, uint64_t len,
+                       float* out, uint32_t ctas, void* stream);
+
 /* require_finite (vec.cpp:7-16) on its own: latches the first non-finite index */
 int dmb_require_finite(dmb_ctx* ctx, const float* v, uint64_t n, void* stream);
 
@@ -287,6 +294,10 @@ int dmb_latch_import(dmb_ctx* ctx, const int32_t* d_flag, void* stream);
  * tensor-core step kernel on its stream; read returns their summed time and count
  * (synchronizing on the recorded events) and clears them */
 int dmb_kernel_timer_enable(int on);
+/* process-wide: SMs the persistent tensor-core step kernels leave free for kernels that run
+ * beside them (dmb_grad_mean_pull of the next bucket); 0 (default) uses every SM.  The
+ * environment variable DMB_SM_RESERVE overrides it. */
+int dmb_set_sm_reserve(int sms);
 int dmb_kernel_timer_read(double* total_ms, uint64_t* launches);
 
 #ifdef __cplusplus

@@ -301,7 +301,8 @@ class HybridCluster:
 
     def __init__(self, topo: Topology, param_count: int, opt: OptimizerConfig, rep: ReplicatorConfig,
                  initial_params: torch.Tensor, rank: int, shard_group=None, replica_group=None,
-                 buckets: int = 8, wire: str = "mask", exchange=None, world_group=None, trace: bool = False):
+                 buckets: int = 8, wire: str = "mask", exchange=None, world_group=None, trace: bool = False,
+                 pull_grads: bool = False, pull_ctas: int = 32):
         self.topo, self.opt, self.rep = topo, opt, rep
         self.rank = rank
         self.node, self.accel = divmod(rank, topo.accels_per_node)
@@ -336,8 +337,11 @@ class HybridCluster:
             raise ConfigError(f"unknown exchange layout {wire!r}")
         self.wire = wire
         # buckets: chunk-aligned slices of the shard (DeMo), one bucket for the other schemes
+        # pulled reduce-scatter (A > 1): the members' full gradients live in symmetric memory and
+        # every rank pulls its shard's slices over NVLink bucket by bucket, under the step kernels
+        self.pull = bool(pull_grads) and A > 1 and shard_group is not None
         tile = 128 * max(rep.chunk_size, 1)
-        nb = buckets if (rep.scheme == Scheme.DeMo and R > 1) else 1
+        nb = buckets if (rep.scheme == Scheme.DeMo and (R > 1 or self.pull)) else 1
         edges = sorted({min(L, (L * b // nb) // tile * tile) for b in range(nb)} | {L})
         self.buckets = [dict(lo=lo, hi=hi) for lo, hi in zip(edges[:-1], edges[1:])] if L else []
         # the payload layout of every bucket, from the library, before anything runs
@@ -384,6 +388,8 @@ class HybridCluster:
         self.ce = exchange if isinstance(exchange, CopyEngineExchange) else None
         if isinstance(exchange, LocalExchange):
             exchange.hub.members[rank] = self
+        if self.pull:
+            self._setup_pull(shard_group, pull_ctas)
 
     def _default_exchange(self, shard_group, replica_group, world_group):
         R, A = self.topo.nodes, self.topo.accels_per_node
@@ -408,7 +414,13 @@ class HybridCluster:
         self._tr, self._step, self._lr = tr, step, float(lr)
         self._steps0 = self.steps
         # the pad tail never leaves the node (cluster.cpp:201)
-        self.g_shard = grad_full[:L] if A == 1 else self.exchange.reduce_scatter(self.shard_grad, grad_full)[:L]
+        pulled = self.pull and any(grad_full.data_ptr() == b.data_ptr() for b in self._gbufs)
+        if pulled:
+            self.g_shard = self.shard_grad[:L]
+            self._pull_start(grad_full)
+        else:
+            self._pulled = None
+            self.g_shard = grad_full[:L] if A == 1 else self.exchange.reduce_scatter(self.shard_grad, grad_full)[:L]
         self._pending = []
         if not L:
             return
@@ -416,7 +428,11 @@ class HybridCluster:
         st = _stream(self.g_shard)
         c, o = self.rep.c(), self.opt.c()
         if self.fused:
-            self._fused(ctx, c, o, st)
+            try:
+                self._fused(ctx, c, o, st)
+            finally:
+                if self._pulled:
+                    lib.dmb_set_sm_reserve(0)
         elif self.window < len(self.buckets):
             self._windowed(ctx, c, o, st)
             return
@@ -426,6 +442,7 @@ class HybridCluster:
             try:
                 for bi, b in enumerate(self.buckets):
                     lo, hi = b["lo"], b["hi"]
+                    self._pull_wait(bi)
                     hdr = _capi.Update()
                     hdr.body = self.exchange.own(bi).data_ptr()
                     tb = self._trace_bufs if trace is not None else None
@@ -448,6 +465,8 @@ class HybridCluster:
                     self._pending.append((b, hdr, handle))
             finally:
                 lib.dmb_set_wire_format(ctx, 0)
+                if self._pulled:
+                    lib.dmb_set_sm_reserve(0)
             if trace is not None:
                 if self._trace_bufs is None:
                     raise ConfigError("a traced step needs a DemoSgd member built with trace=True")
@@ -562,6 +581,9 @@ class HybridCluster:
         """memory-bounded step: agree on the finiteness of the whole shard first, then prepare,
         exchange and merge the buckets `window` at a time through the reused slots"""
         L = self.spec.real_len
+        if self._pulled:
+            self._pull_wait(len(self._pulled) - 1)
+            lib.dmb_set_sm_reserve(0)  # the pull is complete before the windows run
         _check(lib.dmb_require_finite(ctx, _ptr(self.g_shard), L, st))
         _check(lib.dmb_latch_export(ctx, _ptr(self.flag), st))
         self.exchange.agree(self.flag)
@@ -594,16 +616,95 @@ class HybridCluster:
                 self.exp_avg_sq, self._es_next = self._es_next, self.exp_avg_sq
 
     def _fused(self, ctx, c, o, st) -> None:
-        """R = 1: prepare -> merge(R = 1) -> apply in one pass (dmb_step_*_local) into the spares"""
-        L, step, lr = self.spec.real_len, self._step, self._lr
-        if self.sgd:
-            _check(lib.dmb_step_sgd_local(ctx, _ptr(self.g_shard), _ptr(self.m), _ptr(self._m_next),
-                                          _ptr(self.params), _ptr(self._p_next), L, C.byref(o), C.byref(c), step,
-                                          self.accel, lr, None, st))
-        else:
-            steps = C.c_uint64(self.steps)
-            _check(lib.dmb_step_adamw_local(ctx, _ptr(self.g_shard), _ptr(self.params), _ptr(self._p_next),
-                                            _ptr(self.exp_avg), _ptr(self._ea_next), _ptr(self.exp_avg_sq),
-                                            _ptr(self._es_next), C.byref(steps), L, C.byref(o), C.byref(c), step,
-                                            self.accel, lr, None, st))
+        """R = 1: prepare -> merge(R = 1) -> apply in one pass (dmb_step_*_local) into the spares;
+        bucket by bucket behind the pulled reduce-scatter (DeMo's selection is chunk-local)"""
+        step, lr = self._step, self._lr
+        spans = [(b["lo"], b["hi"]) for b in self.buckets] if self._pulled else [(0, self.spec.real_len)]
+        steps = C.c_uint64(self.steps)
+        for bi, (lo, hi) in enumerate(spans):
+            if self._pulled:
+                self._pull_wait(bi)
+            sl = lambda t: _ptr(t[lo:hi])  # noqa: E731
+            if self.sgd:
+                _check(lib.dmb_step_sgd_local(ctx, sl(self.g_shard), sl(self.m), sl(self._m_next), sl(self.params),
+                                              sl(self._p_next), hi - lo, C.byref(o), C.byref(c), step, self.accel, lr,
+                                              None, st))
+            else:
+                steps = C.c_uint64(self.steps)  # every bucket advances the counter from the same value
+                _check(lib.dmb_step_adamw_local(ctx, sl(self.g_shard), sl(self.params), sl(self._p_next),
+                                                sl(self.exp_avg), sl(self._ea_next), sl(self.exp_avg_sq),
+                                                sl(self._es_next), C.byref(steps), hi - lo, C.byref(o), C.byref(c),
+                                                step, self.accel, lr, None, st))
+        if not self.sgd:
             self.steps = int(steps.value)
+
+    # ---- pulled reduce-scatter (cluster.cpp:63-91 over NVLink peer memory) --------------------
+    def _setup_pull(self, shard_group, ctas: int) -> None:
+        """two symmetric gradient buffers per rank (the step's parity picks one, so a member's next
+        gradient never overwrites one a peer is still pulling), mapped into every shard-group member"""
+        import torch.distributed._symmetric_memory as symm
+
+        A = self.topo.accels_per_node
+        padded = self.spec.extent * A
+        self._gbufs = [symm.empty(padded, dtype=torch.float32, device=self.device) for _ in range(2)]
+        self._ghdls = [symm.rendezvous(b, shard_group) for b in self._gbufs]
+        if self._ghdls[0].world_size != A or self._ghdls[0].rank != self.accel:
+            raise RuntimeError("symmetric-memory rendezvous does not match the shard group")
+        # every member's buffer as mapped here (peer memory over NVLink for a != accel)
+        self._gview = [[h.get_buffer(a, (padded,), torch.float32, 0) for a in range(A)] for h in self._ghdls]
+        # SM loads of peer memory are round-trip bound (~3 GB/s per CTA measured on B200, against
+        # ~0.5 TB/s for NCCL's stores): the peers' slices are pulled by the copy engines into local
+        # staging, and the member-order mean reads only local memory
+        self._gstage = {a: torch.empty(self.spec.extent, dtype=torch.float32, device=self.device)
+                        for a in range(A) if a != self.accel}
+        self._pull_stream = torch.cuda.Stream(self.device)  # the member-order means
+        self._copy_stream = torch.cuda.Stream(self.device)  # the copy-engine pulls, a bucket ahead of the means
+        self._pull_ctas = int(ctas)
+        self._pulled = None
+
+    def grad_buffer(self, step: int) -> torch.Tensor:
+        """where this rank writes its full (padded) gradient for `step` to take the pulled
+        reduce-scatter (HybridCluster(pull_grads=True)); any other tensor takes the NCCL one"""
+        if not self.pull:
+            raise ConfigError("grad_buffer needs HybridCluster(pull_grads=True) with accels_per_node > 1")
+        return self._gbufs[step & 1]
+
+    def _pull_start(self, grad_full: torch.Tensor) -> None:
+        """after a device barrier of the shard group (every member's gradient is written), per
+        bucket on the side stream: the copy engines pull the peers' slices of this rank's shard over
+        NVLink, then the member-order mean (dmb_grad_mean_pull, a few CTAs, local reads only), an
+        event the bucket's prepare waits on"""
+        A = self.topo.accels_per_node
+        which = 0 if grad_full.data_ptr() == self._gbufs[0].data_ptr() else 1
+        hdl, views = self._ghdls[which], self._gview[which]
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(self.device))
+        self._copy_stream.wait_event(ready)
+        ctx = context(self.device).h
+        sp = C.c_void_p(self._pull_stream.cuda_stream)
+        off0 = self.accel * self.spec.extent
+        spans = [(b["lo"], b["hi"]) for b in self.buckets] or [(0, self.spec.real_len)]
+        copied = []
+        with torch.cuda.stream(self._copy_stream):
+            hdl.barrier(channel=1)  # every member's gradient of this step is written
+            for lo, hi in spans:
+                for a, stg in self._gstage.items():
+                    stg[lo:hi].copy_(views[a][off0 + lo:off0 + hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self._copy_stream)
+                copied.append(ev)
+        events = []
+        for (lo, hi), cev in zip(spans, copied):
+            self._pull_stream.wait_event(cev)
+            srcs = [grad_full[off0 + lo:] if a == self.accel else self._gstage[a][lo:] for a in range(A)]
+            ptrs = (C.c_void_p * A)(*[t.data_ptr() for t in srcs])
+            _check(lib.dmb_grad_mean_pull(ctx, ptrs, A, hi - lo, _ptr(self.shard_grad[lo:hi]), self._pull_ctas, sp))
+            ev = torch.cuda.Event()
+            ev.record(self._pull_stream)
+            events.append(ev)
+        self._pulled = events
+        lib.dmb_set_sm_reserve(self._pull_ctas)  # the step kernels launched in begin leave the pull its SMs
+
+    def _pull_wait(self, bi: int) -> None:
+        if self._pulled:
+            torch.cuda.current_stream(self.device).wait_event(self._pulled[min(bi, len(self._pulled) - 1)])

@@ -21,6 +21,8 @@
 namespace dmb {
 static std::atomic<uint64_t> g_launches{0};
 void count_launches(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+static std::atomic<int> g_sm_reserve{0};
+int sm_reserve() { return g_sm_reserve.load(std::memory_order_relaxed); }
 
 namespace {
 std::mutex g_timer_mu;
@@ -1029,6 +1031,16 @@ int dmb_grad_mean(dmb_ctx* ctx, const float* const* grads, uint64_t members, uin
   return last_launch();
 }
 
+int dmb_grad_mean_pull(dmb_ctx* ctx, const float* const* grads, uint64_t members, uint64_t len, float* out,
+                       uint32_t ctas, void* stream) {
+  (void)ctx;
+  if (members == 0) return fail(DMB_PROTOCOL, "reduce-scatter over an empty group");
+  if (members > (uint64_t)kMaxReplicas) return fail(DMB_PROTOCOL, "too many members");
+  if (!len) return DMB_OK;
+  launch_grad_mean_pull(grads, (int)members, len, out, (int)ctas, as_stream(stream));
+  return last_launch();
+}
+
 int dmb_require_finite(dmb_ctx* ctx, const float* v, uint64_t n, void* stream) {
   if (!n) return DMB_OK;
   launch_check_finite(v, n, ctx->status, as_stream(stream));
@@ -1253,6 +1265,12 @@ int dmb_debug_mt_jump_check(uint64_t engine_seed, uint64_t b) {
 
 // tuning hook (not in the public header): device buffer of 32 x 16 u64 timestamps
 void dmb_debug_events(unsigned long long* d_buf) { g_dbg = d_buf; }
+
+int dmb_set_sm_reserve(int sms) {
+  if (sms < 0) return fail(DMB_CONFIG, "negative SM reserve");
+  g_sm_reserve.store(sms, std::memory_order_relaxed);
+  return DMB_OK;
+}
 
 int dmb_kernel_timer_enable(int on) {
   std::lock_guard<std::mutex> l(g_timer_mu);

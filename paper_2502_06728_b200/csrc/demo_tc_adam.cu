@@ -1884,10 +1884,11 @@ void launch_wire(const ChunkArgs& a, const TensorMaps& maps, cudaStream_t stream
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t ntiles = (a.geo.nchunks + TM - 1) / TM;
-  // DMB_SM_RESERVE=n leaves n SMs to kernels that must run concurrently (the NCCL
-  // all-gather of the previous bucket in the cluster pipeline)
+  // dmb_set_sm_reserve(n) (or DMB_SM_RESERVE=n) leaves n SMs to kernels that must run
+  // concurrently (the pulled reduce-scatter of the next bucket, an NCCL all-gather)
   const char* rs = std::getenv("DMB_SM_RESERVE");
-  const int reserve = rs ? std::atoi(rs) : 0;
+  const int env = rs ? std::atoi(rs) : 0;
+  const int reserve = env > sm_reserve() ? env : sm_reserve();
   if (reserve > 0 && reserve < sms) sms -= reserve;
   const unsigned grid = (unsigned)(ntiles < (uint64_t)sms ? (ntiles ? ntiles : 1) : sms);
   kern<<<grid, THREADS, SMEM_BYTES, stream>>>(a, maps);

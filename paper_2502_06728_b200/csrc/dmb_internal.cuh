@@ -12,6 +12,7 @@ namespace dmb {
 
 // kernels launched through this library (the bench's gpu_launches evidence)
 void count_launches(int n);
+int sm_reserve();  // SMs the persistent step kernels leave free (dmb_set_sm_reserve)
 // dmb_kernel_timer_*: events around the dominant tensor-core kernel's launches
 void timer_begin(cudaStream_t stream);
 void timer_end(cudaStream_t stream);
@@ -218,6 +219,8 @@ void launch_baseline_sgd(float* p, float* m, const float* g, uint64_t n, float b
 void launch_check_finite(const float* g, uint64_t n, DevStatus* st, cudaStream_t stream);
 void launch_grad_mean(const float* const* grads, int members, uint64_t n, float* out,
                       cudaStream_t stream);
+void launch_grad_mean_pull(const float* const* grads, int members, uint64_t n, float* out, int ctas,
+                           cudaStream_t stream);
 void launch_striding_iota(uint32_t* out, uint64_t offset, uint64_t period, uint64_t count,
                           cudaStream_t stream);
 void launch_unpack_values(const uint8_t* vals, uint64_t n, int dtype, float* out,

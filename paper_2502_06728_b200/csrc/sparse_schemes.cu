@@ -438,6 +438,71 @@ __global__ void grad_mean_kernel(GradPtrs gp, int members, uint64_t n, float* __
   }
 }
 
+// grad_reduce_scatter's member-order mean (vec.cpp:18-26, cluster.cpp:63-91) with a CTA budget: a
+// persistent grid of `ctas` CTAs that can run beside a step kernel leaving those SMs free (the
+// cluster's reduce-scatter of bucket b+1 under the prepare of bucket b).  Few CTAs must still move
+// HBM-rate bytes, so the latency is hidden by loads in flight, not by occupancy: every thread
+// issues kPullUnroll 16-byte loads of every member (the member count a template parameter for
+// 2-4) before summing them -- from 0, members in order, then divided, as mean_of does.
+constexpr int kPullThreads = 512;
+constexpr int kPullUnroll = 8;
+
+template <int M>  // members; 0: run-time count
+__global__ void __launch_bounds__(kPullThreads) grad_mean_pull_kernel(GradPtrs gp, int members, uint64_t n4,
+                                                                      float4* __restrict__ out) {
+  const int nm = M > 0 ? M : members;
+  const float inv = (float)nm;
+  const uint64_t stride = (uint64_t)gridDim.x * kPullThreads;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * kPullThreads + threadIdx.x; i0 < n4; i0 += stride * kPullUnroll) {
+    float4 acc[kPullUnroll];
+#pragma unroll
+    for (int u = 0; u < kPullUnroll; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (M > 0) {
+      float4 v[M > 0 ? M : 1][kPullUnroll];
+#pragma unroll
+      for (int a = 0; a < (M > 0 ? M : 1); ++a) {
+        const float4* src = reinterpret_cast<const float4*>(gp.p[a]);
+#pragma unroll
+        for (int u = 0; u < kPullUnroll; ++u) {
+          const uint64_t i = i0 + u * stride;
+          v[a][u] = i < n4 ? __ldcg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < (M > 0 ? M : 1); ++a)
+#pragma unroll
+        for (int u = 0; u < kPullUnroll; ++u) {
+          acc[u].x += v[a][u].x;
+          acc[u].y += v[a][u].y;
+          acc[u].z += v[a][u].z;
+          acc[u].w += v[a][u].w;
+        }
+    } else {
+      for (int a = 0; a < nm; ++a) {
+        const float4* src = reinterpret_cast<const float4*>(gp.p[a]);
+        float4 v[kPullUnroll];
+#pragma unroll
+        for (int u = 0; u < kPullUnroll; ++u) {
+          const uint64_t i = i0 + u * stride;
+          v[u] = i < n4 ? __ldcg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kPullUnroll; ++u) {
+          acc[u].x += v[u].x;
+          acc[u].y += v[u].y;
+          acc[u].z += v[u].z;
+          acc[u].w += v[u].w;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kPullUnroll; ++u) {
+      const uint64_t i = i0 + u * stride;
+      if (i < n4) out[i] = make_float4(acc[u].x / inv, acc[u].y / inv, acc[u].z / inv, acc[u].w / inv);
+    }
+  }
+}
+
 __global__ void unpack_values_kernel(const uint8_t* __restrict__ vals, uint64_t n, int dtype,
                                      float* __restrict__ out) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -557,6 +622,39 @@ void launch_grad_mean(const float* const* grads, int members, uint64_t n, float*
   GradPtrs gp{};
   for (int a = 0; a < members && a < kMaxReplicas; ++a) gp.p[a] = grads[a];
   grad_mean_kernel<<<grid_for(n), kBlock, 0, stream>>>(gp, members, n, out);
+}
+
+void launch_grad_mean_pull(const float* const* grads, int members, uint64_t n, float* out, int ctas,
+                           cudaStream_t stream) {
+  GradPtrs gp{};
+  bool al = (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+  for (int a = 0; a < members && a < kMaxReplicas; ++a) {
+    gp.p[a] = grads[a];
+    al = al && (reinterpret_cast<uintptr_t>(grads[a]) & 15u) == 0;
+  }
+  const uint64_t n4 = al ? n / 4 : 0;
+  if (n4) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t want = (n4 + (uint64_t)kPullThreads * kPullUnroll - 1) / ((uint64_t)kPullThreads * kPullUnroll);
+    const uint64_t cap = (uint64_t)(ctas > 0 ? ctas : sms);
+    count_launches(1);
+    const unsigned grid = (unsigned)(want < cap ? want : cap);
+    float4* o4 = reinterpret_cast<float4*>(out);
+    switch (members) {
+      case 2: grad_mean_pull_kernel<2><<<grid, kPullThreads, 0, stream>>>(gp, members, n4, o4); break;
+      case 3: grad_mean_pull_kernel<3><<<grid, kPullThreads, 0, stream>>>(gp, members, n4, o4); break;
+      case 4: grad_mean_pull_kernel<4><<<grid, kPullThreads, 0, stream>>>(gp, members, n4, o4); break;
+      default: grad_mean_pull_kernel<0><<<grid, kPullThreads, 0, stream>>>(gp, members, n4, o4);
+    }
+  }
+  if (n4 * 4 < n) {  // the tail, or every element of a misaligned vector
+    GradPtrs gt{};
+    for (int a = 0; a < members && a < kMaxReplicas; ++a) gt.p[a] = grads[a] + n4 * 4;
+    count_launches(1);
+    grad_mean_kernel<<<grid_for(n - n4 * 4), kBlock, 0, stream>>>(gt, members, n - n4 * 4, out + n4 * 4);
+  }
 }
 
 void launch_unpack_values(const uint8_t* vals, uint64_t n, int dtype, float* out,
