@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--pull-rs", type=int, default=1,
                     help="S>1: the gradients live in symmetric memory and every rank pulls its shard over NVLink "
                          "bucket by bucket under the step kernels (0: NCCL reduce-scatter)")
+    ap.add_argument("--pull-ctas", type=int, default=40, help="SMs the pulled reduce-scatter's mean kernel runs on")
     ap.add_argument("--grad-ring", type=int, default=3, help="pre-generated gradients, one per step in turn")
     return ap.parse_args()
 
@@ -281,7 +282,7 @@ def run_ours(args, rank, world, local_rank):
         sg, rg = groups_for(topo, rank)
         os.environ["DMB_SM_RESERVE"] = str(args.sm_reserve)
         cluster = HybridCluster(topo, L, opt, cfg, params, rank, sg, rg, buckets=args.buckets, wire=args.wire,
-                                pull_grads=bool(args.pull_rs) and S > 1)
+                                pull_grads=bool(args.pull_rs) and S > 1, pull_ctas=args.pull_ctas)
         del params
         if cluster.pull:  # the ring is the two symmetric gradient buffers, alternating by step
             grads = [cluster.grad_buffer(i).normal_(0.0, 1e-3, generator=gen) for i in range(2)]

@@ -302,7 +302,7 @@ class HybridCluster:
     def __init__(self, topo: Topology, param_count: int, opt: OptimizerConfig, rep: ReplicatorConfig,
                  initial_params: torch.Tensor, rank: int, shard_group=None, replica_group=None,
                  buckets: int = 8, wire: str = "mask", exchange=None, world_group=None, trace: bool = False,
-                 pull_grads: bool = False, pull_ctas: int = 32):
+                 pull_grads: bool = False, pull_ctas: int = 40):
         self.topo, self.opt, self.rep = topo, opt, rep
         self.rank = rank
         self.node, self.accel = divmod(rank, topo.accels_per_node)
