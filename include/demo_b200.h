@@ -206,6 +206,17 @@ int dmb_merge_apply_adamw(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_up
                           float* exp_avg, float* exp_avg_sq, uint64_t* steps, const float* grad,
                           uint64_t len, uint64_t step, const dmb_opt_cfg* opt, double lr,
                           void* stream);
+/* the same merges with the state read from *_in and written to *_out (distinct buffers: the
+ * step can merge before the ranks have agreed on it, a refused step keeps every *_in; synchronized
+ * updates only) */
+int dmb_merge_apply_sgd_to(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_updates,
+                           const dmb_rep_cfg* cfg, const float* p_in, float* p_out, uint64_t len,
+                           uint64_t step, double lr, void* stream);
+int dmb_merge_apply_adamw_to(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_updates,
+                             uint64_t own_rank, const dmb_rep_cfg* cfg, const float* p_in, float* p_out,
+                             const float* ea_in, float* ea_out, const float* es_in, float* es_out,
+                             uint64_t* steps, const float* grad, uint64_t len, uint64_t step,
+                             const dmb_opt_cfg* opt, double lr, void* stream);
 /* one replica group of one member: prepare -> merge(R=1) -> apply in one pass over HBM.
  * `out` may be NULL (payload not materialized) or receive the update for inspection. */
 /* DeMo scheme only.  State is read from *_in and written to *_out (they may alias;

@@ -120,6 +120,8 @@ _SIGS = {
     "dmb_extract_fast_components": (C.c_int, [P, P, U64, U64, U64, P, P, P, P, P]),
     "dmb_sign_transform": (C.c_int, [P, P, U64, P]),
     "dmb_grad_mean_pull": (C.c_int, [P, P, U64, U64, P, C.c_uint32, P]),
+    "dmb_merge_apply_sgd_to": (C.c_int, [P, P, U64, P, P, P, U64, U64, C.c_double, P]),
+    "dmb_merge_apply_adamw_to": (C.c_int, [P, P, U64, U64, P, P, P, P, P, P, P, P, P, U64, U64, P, C.c_double, P]),
     "dmb_set_sm_reserve": (C.c_int, [C.c_int]),
     "dmb_toy_loss_grad": (C.c_int, [P, P, P, P, U64, U64, P, U64, U64, U64, P, U64, P, P]),
     "dmb_toy_loss": (C.c_int, [P, P, P, P, P, P]),

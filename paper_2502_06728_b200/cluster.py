@@ -302,7 +302,8 @@ class HybridCluster:
     def __init__(self, topo: Topology, param_count: int, opt: OptimizerConfig, rep: ReplicatorConfig,
                  initial_params: torch.Tensor, rank: int, shard_group=None, replica_group=None,
                  buckets: int = 8, wire: str = "mask", exchange=None, world_group=None, trace: bool = False,
-                 pull_grads: bool = False, pull_ctas: int = 40):
+                 pull_grads: bool = False, pull_ctas: int = 40, overlap: Optional[bool] = None,
+                 merge_sms: int = 90):
         self.topo, self.opt, self.rep = topo, opt, rep
         self.rank = rank
         self.node, self.accel = divmod(rank, topo.accels_per_node)
@@ -390,6 +391,29 @@ class HybridCluster:
             exchange.hub.members[rank] = self
         if self.pull:
             self._setup_pull(shard_group, pull_ctas)
+        # overlapped merges (opt-in: overlap=True or DMB_OVERLAP=1; R > 1, DeMo, one process per GPU):
+        # the merge of bucket b runs on its own stream and its own SMs while the prepares of the
+        # later buckets run on the rest -- the select-bound encode beside the HBM-bound merge --
+        # writing into spare state buffers, so the step can merge before the ranks agree on it and
+        # a refused step keeps the old state (bit-identical to the sequential step).  Measured on
+        # B200 at 1 x 2 (OLMo-1B AdamW): 11.9 ms at the best split (90 merge SMs) against 11.3 ms
+        # sequential, so it is off by default.  Needs the spares to fit (4 B/param SGD, 12 AdamW).
+        spare = L * (4 if self.sgd else 12)
+        auto = (R > 1 and rep.scheme == Scheme.DeMo and L > 0 and not self.fused and not self.pull and not trace
+                and self.window == len(self.buckets) and not isinstance(exchange, LocalExchange)
+                and torch.cuda.mem_get_info(self.device)[0] > spare + (8 << 30))
+        if overlap is None and os.environ.get("DMB_OVERLAP"):
+            overlap = os.environ["DMB_OVERLAP"] != "0"
+        merge_sms = int(os.environ.get("DMB_MERGE_SMS", merge_sms))
+        self.overlap = bool(overlap) and auto
+        if self.overlap:
+            self._p_next = z()
+            if not self.sgd:
+                self._ea_next, self._es_next = z(), z()
+            self._mstream = torch.cuda.Stream(self.device)
+            sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+            self._m_sms = max(1, min(int(merge_sms), sms - 1))
+            self._e_sms = sms - self._m_sms
 
     def _default_exchange(self, shard_group, replica_group, world_group):
         R, A = self.topo.nodes, self.topo.accels_per_node
@@ -446,6 +470,8 @@ class HybridCluster:
                     hdr = _capi.Update()
                     hdr.body = self.exchange.own(bi).data_ptr()
                     tb = self._trace_bufs if trace is not None else None
+                    if self.overlap:
+                        lib.dmb_set_sm_reserve(self._m_sms)  # the prepares leave the merges their SMs
                     if self.sgd:
                         _check(lib.dmb_demo_sgd_prepare(ctx, _ptr(self.g_shard[lo:hi]), _ptr(self.m[lo:hi]),
                                                         _ptr(self._m_next[lo:hi]), hi - lo, C.byref(o), C.byref(c),
@@ -463,10 +489,15 @@ class HybridCluster:
                                                                         self.rep.transfer_dtype)) * (R - 1)
                     handle = self.exchange.start(bi) if not hdr.empty else None
                     self._pending.append((b, hdr, handle))
+                    if self.overlap:
+                        self._merge_to(ctx, c, o, bi, b, hdr, handle)
             finally:
                 lib.dmb_set_wire_format(ctx, 0)
-                if self._pulled:
+                if self._pulled or self.overlap:
                     lib.dmb_set_sm_reserve(0)
+            if self.overlap:
+                self._mdone = torch.cuda.Event()
+                self._mdone.record(self._mstream)
             if trace is not None:
                 if self._trace_bufs is None:
                     raise ConfigError("a traced step needs a DemoSgd member built with trace=True")
@@ -486,8 +517,12 @@ class HybridCluster:
         if L:
             ctx = context(self.device).h
             st = _stream(self.g_shard)
+            if self.overlap and self._pending:
+                torch.cuda.current_stream(self.device).wait_event(self._mdone)
             _check(lib.dmb_latch_import(ctx, _ptr(self.flag), st))
-            if not self.fused and self._pending:
+            if self.overlap:
+                self.steps = self._steps0 + 1 if not self.sgd else self.steps
+            elif not self.fused and self._pending:
                 c, o = self.rep.c(), self.opt.c()
                 R = self.topo.nodes
                 steps = C.c_uint64(self.steps)
@@ -527,7 +562,18 @@ class HybridCluster:
         """Synchronize; on a refused step undo the buffer swaps and the step counter, then
         raise TrainingError (every state vector is as before the step)."""
         try:
-            status(self.device)
+            try:
+                status(self.device)
+            except ProtocolError:
+                # overlapped merges ran before the agreement: a member that refused the step may
+                # have left bodies that do not parse -- its refusal is the step's outcome
+                if not (self.overlap and int(self.flag.item())):
+                    raise
+                try:
+                    status(self.device)  # consume the refusal latch as well
+                except TrainingError:
+                    pass
+                raise TrainingError("gradient contains a non-finite value (on another rank of the step)") from None
         except TrainingError:
             self._swap()  # back to the buffers of the last good step
             self.steps = self._steps0
@@ -577,6 +623,30 @@ class HybridCluster:
                                              _ptr(self.g_shard[lo:hi]), hi - lo, self._step, C.byref(o), self._lr,
                                              st))
 
+    def _merge_to(self, ctx, c, o, bi, b, hdr, handle) -> None:
+        """bucket bi's merge + apply on the merge stream, into the spare state buffers, once its
+        exchange has landed (overlapped mode)"""
+        lo, hi = b["lo"], b["hi"]
+        R = self.topo.nodes
+        with torch.cuda.stream(self._mstream):
+            ptrs = self.exchange.bodies(bi, handle)  # the merge stream waits for the exchange
+            ups = (_capi.Update * R)()
+            for r in range(R):
+                ups[r] = hdr
+                ups[r].body = ptrs[r]
+            ms = C.c_void_p(self._mstream.cuda_stream)
+            lib.dmb_set_sm_reserve(self._e_sms)  # the merge leaves the prepares their SMs
+            sl = lambda t: _ptr(t[lo:hi])  # noqa: E731
+            if self.sgd:
+                _check(lib.dmb_merge_apply_sgd_to(ctx, ups, R, C.byref(c), sl(self.params), sl(self._p_next), hi - lo,
+                                                  self._step, self._lr, ms))
+            else:
+                steps = C.c_uint64(self._steps0)  # every bucket advances the counter from the same value
+                _check(lib.dmb_merge_apply_adamw_to(ctx, ups, R, self.node, C.byref(c), sl(self.params),
+                                                    sl(self._p_next), sl(self.exp_avg), sl(self._ea_next),
+                                                    sl(self.exp_avg_sq), sl(self._es_next), C.byref(steps),
+                                                    sl(self.g_shard), hi - lo, self._step, C.byref(o), self._lr, ms))
+
     def _windowed(self, ctx, c, o, st) -> None:
         """memory-bounded step: agree on the finiteness of the whole shard first, then prepare,
         exchange and merge the buckets `window` at a time through the reused slots"""
@@ -609,7 +679,7 @@ class HybridCluster:
             return
         if self.sgd:
             self.m, self._m_next = self._m_next, self.m
-        if self.fused:
+        if self.fused or self.overlap:
             self.params, self._p_next = self._p_next, self.params
             if not self.sgd:
                 self.exp_avg, self._ea_next = self._ea_next, self.exp_avg

@@ -865,16 +865,51 @@ int dmb_baseline_sgd_step(dmb_ctx* ctx, float* params, float* m, const float* gr
   return last_launch();
 }
 
+namespace {
+int merge_sgd(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_updates, const dmb_rep_cfg* cfg,
+              const float* p_in, float* params, uint64_t len, double lr, cudaStream_t s);
+int merge_adamw(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_updates, uint64_t own_rank,
+                const dmb_rep_cfg* cfg, const float* p_in, float* p_out, const float* ea_in, float* ea_out,
+                const float* es_in, float* es_out, uint64_t* steps, const float* grad, uint64_t len,
+                const dmb_opt_cfg* opt, double lr, cudaStream_t s);
+}  // namespace
+
 int dmb_merge_apply_sgd(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_updates,
                         const dmb_rep_cfg* cfg, float* params, const float* grad_if_unsynced,
                         uint64_t len, uint64_t step, double lr, void* stream) {
-  cudaStream_t s = as_stream(stream);
   (void)step;
   if (!updates || n_updates == 0 || updates[0].empty) {
     // DiLoCo between beats: SGD steps on the raw shard gradient (cluster.cpp:225)
     if (!grad_if_unsynced) return fail(DMB_PROTOCOL, "unsynced step needs the local gradient");
     return dmb_demo_sgd_apply(ctx, params, grad_if_unsynced, len, lr, stream);
   }
+  return merge_sgd(ctx, updates, n_updates, cfg, params, params, len, lr, as_stream(stream));
+}
+
+int dmb_merge_apply_sgd_to(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_updates,
+                           const dmb_rep_cfg* cfg, const float* p_in, float* p_out, uint64_t len,
+                           uint64_t step, double lr, void* stream) {
+  (void)step;
+  if (!updates || n_updates == 0 || updates[0].empty)
+    return fail(DMB_PROTOCOL, "the out-of-place merge needs synchronized updates");
+  return merge_sgd(ctx, updates, n_updates, cfg, p_in, p_out, len, lr, as_stream(stream));
+}
+
+int dmb_merge_apply_adamw_to(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_updates,
+                             uint64_t own_rank, const dmb_rep_cfg* cfg, const float* p_in, float* p_out,
+                             const float* ea_in, float* ea_out, const float* es_in, float* es_out,
+                             uint64_t* steps, const float* grad, uint64_t len, uint64_t step,
+                             const dmb_opt_cfg* opt, double lr, void* stream) {
+  (void)step;
+  if (!updates || n_updates == 0 || updates[0].empty)
+    return fail(DMB_PROTOCOL, "the out-of-place merge needs synchronized updates");
+  return merge_adamw(ctx, updates, n_updates, own_rank, cfg, p_in, p_out, ea_in, ea_out, es_in, es_out, steps,
+                     grad, len, opt, lr, as_stream(stream));
+}
+
+namespace {
+int merge_sgd(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_updates, const dmb_rep_cfg* cfg,
+              const float* p_in, float* params, uint64_t len, double lr, cudaStream_t s) {
   if (int rc = validate_updates(updates, n_updates, cfg)) return rc;
   if (updates[0].length != len) return fail(DMB_PROTOCOL, "update length does not match the shard");
   if (!len) return DMB_OK;
@@ -883,7 +918,7 @@ int dmb_merge_apply_sgd(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_upda
     a.geo = geometry(cfg, len);
     if (int rc = get_basis(ctx, a.geo.s, &a.basis)) return rc;
     a.in = bodies_of(updates, n_updates, false);
-    a.p_in = params;
+    a.p_in = p_in;
     a.p_out = params;
     a.sgd = sgd_scalars(0.0, lr);
     a.status = ctx->status;
@@ -899,23 +934,32 @@ int dmb_merge_apply_sgd(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_upda
   SparseSel sel;
   if (int rc = sparse_sel(ctx, cfg, &updates[0], &sel, s)) return rc;
   launch_sparse_merge_apply(sel, bodies_of(updates, n_updates, true), cfg->transfer_dtype,
-                            kMergeSgd, nullptr, params, params, nullptr, nullptr, nullptr, nullptr,
+                            kMergeSgd, nullptr, p_in, params, nullptr, nullptr, nullptr, nullptr,
                             nullptr, sgd_scalars(0.0, lr), AdamScalars{}, ctx->status, s);
   return last_launch();
 }
+}  // namespace
 
 int dmb_merge_apply_adamw(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_updates,
                           uint64_t own_rank, const dmb_rep_cfg* cfg, float* params,
                           float* exp_avg, float* exp_avg_sq, uint64_t* steps, const float* grad,
                           uint64_t len, uint64_t step, const dmb_opt_cfg* opt, double lr,
                           void* stream) {
-  cudaStream_t s = as_stream(stream);
   (void)step;
   if (!updates || n_updates == 0 || updates[0].empty) {
     // merged == nullptr: AdamW on the raw local gradient (cluster.cpp:227, optim.cpp:65)
     return dmb_adamw_apply(ctx, params, exp_avg, exp_avg_sq, steps, grad, grad, nullptr, len, opt,
                            lr, stream);
   }
+  return merge_adamw(ctx, updates, n_updates, own_rank, cfg, params, params, exp_avg, exp_avg, exp_avg_sq,
+                     exp_avg_sq, steps, grad, len, opt, lr, as_stream(stream));
+}
+
+namespace {
+int merge_adamw(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_updates, uint64_t own_rank,
+                const dmb_rep_cfg* cfg, const float* p_in, float* params, const float* ea_in, float* exp_avg,
+                const float* es_in, float* exp_avg_sq, uint64_t* steps, const float* grad, uint64_t len,
+                const dmb_opt_cfg* opt, double lr, cudaStream_t s) {
   if (int rc = validate_updates(updates, n_updates, cfg)) return rc;
   if (updates[0].length != len) return fail(DMB_PROTOCOL, "update length does not match the shard");
   if (own_rank >= n_updates) return fail(DMB_PROTOCOL, "own rank outside the replica group");
@@ -929,11 +973,11 @@ int dmb_merge_apply_adamw(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_up
     a.in = bodies_of(updates, n_updates, false);
     a.own_rank = (int)own_rank;
     a.g = grad;
-    a.p_in = params;
+    a.p_in = p_in;
     a.p_out = params;
-    a.ea_in = exp_avg;
+    a.ea_in = ea_in;
     a.ea_out = exp_avg;
-    a.es_in = exp_avg_sq;
+    a.es_in = es_in;
     a.es_out = exp_avg_sq;
     a.adam = A;
     a.status = ctx->status;
@@ -949,10 +993,11 @@ int dmb_merge_apply_adamw(dmb_ctx* ctx, const dmb_update* updates, uint64_t n_up
   SparseSel sel;
   if (int rc = sparse_sel(ctx, cfg, &updates[0], &sel, s)) return rc;
   launch_sparse_merge_apply(sel, bodies_of(updates, n_updates, true), cfg->transfer_dtype,
-                            kMergeAdam, grad, params, params, exp_avg, exp_avg, exp_avg_sq,
+                            kMergeAdam, grad, p_in, params, ea_in, exp_avg, es_in,
                             exp_avg_sq, nullptr, SgdScalars{}, A, ctx->status, s);
   return last_launch();
 }
+}  // namespace
 
 int dmb_step_sgd_local(dmb_ctx* ctx, const float* grad, const float* m_in, float* m_out,
                        const float* p_in, float* p_out, uint64_t len, const dmb_opt_cfg* opt,
