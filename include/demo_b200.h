@@ -242,6 +242,31 @@ int dmb_grad_mean(dmb_ctx* ctx, const float* const* grads, uint64_t members, uin
 int dmb_grad_mean_pull(dmb_ctx* ctx, const float* const* grads, uint64_t members, uint64_t len,
                        float* out, uint32_t ctas, void* stream);
 
+/* The shard group's reduce-scatter fused into the prepare / the one-member step: the encoded
+ * gradient is the member-order mean of members[0..n) (mean_of, vec.cpp:18-26 -- each a
+ * shard-sized slice of a member's gradient, local or staged from a peer), computed in the
+ * tensor-core kernel's gradient load and written to grad_mean for the later readers (the merge
+ * re-derives local_q from it).  The AdamW prepare takes four members, the other three two;
+ * otherwise (and on the generic kernels) the mean is a pass of its own first. */
+int dmb_adamw_prepare_members(dmb_ctx* ctx, const float* const* members, uint32_t n_members,
+                              float* grad_mean, uint64_t len, const dmb_rep_cfg* cfg, uint64_t step,
+                              uint32_t shard, dmb_update* out, void* stream);
+int dmb_demo_sgd_prepare_members(dmb_ctx* ctx, const float* const* members, uint32_t n_members,
+                                 float* grad_mean, const float* m_in, float* m_out, uint64_t len,
+                                 const dmb_opt_cfg* opt, const dmb_rep_cfg* cfg, uint64_t step,
+                                 uint32_t shard, dmb_update* out, void* stream);
+int dmb_step_sgd_local_members(dmb_ctx* ctx, const float* const* members, uint32_t n_members,
+                               float* grad_mean, const float* m_in, float* m_out, const float* p_in,
+                               float* p_out, uint64_t len, const dmb_opt_cfg* opt,
+                               const dmb_rep_cfg* cfg, uint64_t step, uint32_t shard, double lr,
+                               dmb_update* out, void* stream);
+int dmb_step_adamw_local_members(dmb_ctx* ctx, const float* const* members, uint32_t n_members,
+                                 float* grad_mean, const float* p_in, float* p_out,
+                                 const float* ea_in, float* ea_out, const float* es_in,
+                                 float* es_out, uint64_t* steps, uint64_t len,
+                                 const dmb_opt_cfg* opt, const dmb_rep_cfg* cfg, uint64_t step,
+                                 uint32_t shard, double lr, dmb_update* out, void* stream);
+
 /* require_finite (vec.cpp:7-16) on its own: latches the first non-finite index */
 int dmb_require_finite(dmb_ctx* ctx, const float* v, uint64_t n, void* stream);
 

@@ -123,6 +123,12 @@ _SIGS = {
     "dmb_merge_apply_sgd_to": (C.c_int, [P, P, U64, P, P, P, U64, U64, C.c_double, P]),
     "dmb_merge_apply_adamw_to": (C.c_int, [P, P, U64, U64, P, P, P, P, P, P, P, P, P, U64, U64, P, C.c_double, P]),
     "dmb_set_sm_reserve": (C.c_int, [C.c_int]),
+    "dmb_demo_sgd_prepare_members": (C.c_int, [P, P, C.c_uint32, P, P, P, U64, P, P, U64, C.c_uint32, P, P]),
+    "dmb_step_sgd_local_members": (C.c_int, [P, P, C.c_uint32, P, P, P, P, P, U64, P, P, U64, C.c_uint32,
+                                             C.c_double, P, P]),
+    "dmb_adamw_prepare_members": (C.c_int, [P, P, C.c_uint32, P, U64, P, U64, C.c_uint32, P, P]),
+    "dmb_step_adamw_local_members": (C.c_int, [P, P, C.c_uint32, P, P, P, P, P, P, P, P, U64, P, P, U64,
+                                               C.c_uint32, C.c_double, P, P]),
     "dmb_toy_loss_grad": (C.c_int, [P, P, P, P, U64, U64, P, U64, U64, U64, P, U64, P, P]),
     "dmb_toy_loss": (C.c_int, [P, P, P, P, P, P]),
     "dmb_latch_export": (C.c_int, [P, P, P]),

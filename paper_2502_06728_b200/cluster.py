@@ -472,12 +472,23 @@ class HybridCluster:
                     tb = self._trace_bufs if trace is not None else None
                     if self.overlap:
                         lib.dmb_set_sm_reserve(self._m_sms)  # the prepares leave the merges their SMs
-                    if self.sgd:
+                    if self.sgd and self._pulled and self._pull_fused:  # the shard's mean fused into the prepare
+                        srcs = self._members_at(lo)
+                        _check(lib.dmb_demo_sgd_prepare_members(ctx, srcs, len(srcs), _ptr(self.g_shard[lo:hi]),
+                                                                _ptr(self.m[lo:hi]), _ptr(self._m_next[lo:hi]),
+                                                                hi - lo, C.byref(o), C.byref(c), step, self.accel,
+                                                                C.byref(hdr), st))
+                    elif self.sgd:
                         _check(lib.dmb_demo_sgd_prepare(ctx, _ptr(self.g_shard[lo:hi]), _ptr(self.m[lo:hi]),
                                                         _ptr(self._m_next[lo:hi]), hi - lo, C.byref(o), C.byref(c),
                                                         step, self.accel, C.byref(hdr),
                                                         _ptr(tb[0][lo:hi]) if tb else None,
                                                         _ptr(tb[1][lo:hi]) if tb else None, st))
+                    elif self._pulled and self._pull_fused:  # the shard's mean fused into the prepare
+                        srcs = self._members_at(lo)
+                        _check(lib.dmb_adamw_prepare_members(ctx, srcs, len(srcs), _ptr(self.g_shard[lo:hi]),
+                                                             hi - lo, C.byref(c), step, self.accel, C.byref(hdr),
+                                                             st))
                     else:
                         _check(lib.dmb_adamw_prepare(ctx, _ptr(self.g_shard[lo:hi]), hi - lo, C.byref(c), step,
                                                      self.accel, C.byref(hdr), None, st))
@@ -654,6 +665,10 @@ class HybridCluster:
         if self._pulled:
             self._pull_wait(len(self._pulled) - 1)
             lib.dmb_set_sm_reserve(0)  # the pull is complete before the windows run
+            if self._pull_fused:  # the windows need the whole shard's mean before the pre-check
+                srcs = self._members_at(0)
+                _check(lib.dmb_grad_mean(ctx, srcs, len(srcs), L, _ptr(self.g_shard), st))
+                self._pull_fused = False
         _check(lib.dmb_require_finite(ctx, _ptr(self.g_shard), L, st))
         _check(lib.dmb_latch_export(ctx, _ptr(self.flag), st))
         self.exchange.agree(self.flag)
@@ -695,10 +710,23 @@ class HybridCluster:
             if self._pulled:
                 self._pull_wait(bi)
             sl = lambda t: _ptr(t[lo:hi])  # noqa: E731
-            if self.sgd:
+            if self.sgd and self._pulled and self._pull_fused:  # the shard's mean fused into the step
+                srcs = self._members_at(lo)
+                _check(lib.dmb_step_sgd_local_members(ctx, srcs, len(srcs), sl(self.g_shard), sl(self.m),
+                                                      sl(self._m_next), sl(self.params), sl(self._p_next), hi - lo,
+                                                      C.byref(o), C.byref(c), step, self.accel, lr, None, st))
+            elif self.sgd:
                 _check(lib.dmb_step_sgd_local(ctx, sl(self.g_shard), sl(self.m), sl(self._m_next), sl(self.params),
                                               sl(self._p_next), hi - lo, C.byref(o), C.byref(c), step, self.accel, lr,
                                               None, st))
+            elif self._pulled and self._pull_fused:  # the shard's mean fused into the step
+                steps = C.c_uint64(self.steps)
+                srcs = self._members_at(lo)
+                _check(lib.dmb_step_adamw_local_members(ctx, srcs, len(srcs), sl(self.g_shard), sl(self.params),
+                                                        sl(self._p_next), sl(self.exp_avg), sl(self._ea_next),
+                                                        sl(self.exp_avg_sq), sl(self._es_next), C.byref(steps),
+                                                        hi - lo, C.byref(o), C.byref(c), step, self.accel, lr, None,
+                                                        st))
             else:
                 steps = C.c_uint64(self.steps)  # every bucket advances the counter from the same value
                 _check(lib.dmb_step_adamw_local(ctx, sl(self.g_shard), sl(self.params), sl(self._p_next),
@@ -731,6 +759,7 @@ class HybridCluster:
         self._copy_stream = torch.cuda.Stream(self.device)  # the copy-engine pulls, a bucket ahead of the means
         self._pull_ctas = int(ctas)
         self._pulled = None
+        self._pull_fused = False
 
     def grad_buffer(self, step: int) -> torch.Tensor:
         """where this rank writes its full (padded) gradient for `step` to take the pulled
@@ -755,14 +784,34 @@ class HybridCluster:
         off0 = self.accel * self.spec.extent
         spans = [(b["lo"], b["hi"]) for b in self.buckets] or [(0, self.spec.real_len)]
         copied = []
+        direct = os.environ.get("DMB_PULL_DIRECT") == "1" and self.rep.scheme == Scheme.DeMo
         with torch.cuda.stream(self._copy_stream):
             hdl.barrier(channel=1)  # every member's gradient of this step is written
             for lo, hi in spans:
+                if direct:  # (experiment) the kernel's TMA reads the peers' slices over NVLink itself
+                    break
                 for a, stg in self._gstage.items():
                     stg[lo:hi].copy_(views[a][off0 + lo:off0 + hi], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(self._copy_stream)
                 copied.append(ev)
+        # AdamW DeMo: the mean is fused into the tensor-core kernel's gradient load (two members
+        # for the one-pass R = 1 step, four for the prepare); the sources, in member order, are
+        # this rank's own slice and the staged ones
+        srcs = [grad_full[off0:] if a == self.accel else (views[a][off0:] if direct else self._gstage[a])
+                for a in range(A)]
+        if direct:
+            ev = torch.cuda.Event()
+            ev.record(self._copy_stream)
+            copied = [ev] * len(spans)
+        self._pull_fused = (self.rep.scheme == Scheme.DeMo
+                            and A <= (4 if not (self.sgd or self.fused) else 2)
+                            and all(t.data_ptr() % 16 == 0 and (4 * b["lo"]) % 16 == 0
+                                    for t in srcs for b in (self.buckets or [dict(lo=0)])))
+        if self._pull_fused:
+            self._pull_srcs = srcs
+            self._pulled = copied
+            return
         events = []
         for (lo, hi), cev in zip(spans, copied):
             self._pull_stream.wait_event(cev)
@@ -774,6 +823,10 @@ class HybridCluster:
             events.append(ev)
         self._pulled = events
         lib.dmb_set_sm_reserve(self._pull_ctas)  # the step kernels launched in begin leave the pull its SMs
+
+    def _members_at(self, lo: int):
+        """the members' slices of this rank's shard from element lo on, in member order"""
+        return (C.c_void_p * len(self._pull_srcs))(*[t.data_ptr() + 4 * lo for t in self._pull_srcs])
 
     def _pull_wait(self, bi: int) -> None:
         if self._pulled:

@@ -543,7 +543,8 @@ void set_mask_header(const dmb_rep_cfg* cfg, dmb_update* out) {
 // Encode one vector (v = g, or m_acc from beta*m_in + g when sgd) into *out.
 int encode(dmb_ctx* ctx, DevStatus* st, bool sgd, const float* g, const float* m_in, float* m_out,
            double beta, uint64_t len, const dmb_rep_cfg* cfg, uint64_t step, uint32_t shard,
-           dmb_update* out, float* local_q, float* m_accum, cudaStream_t s) {
+           dmb_update* out, float* local_q, float* m_accum, cudaStream_t s,
+           const float* const* srcs = nullptr, int n_src = 0) {
   if (!out) return fail(DMB_CONFIG, "update output is NULL");
   if (int rc = plan(cfg, len, step, shard, out)) return rc;
   if (!out->body && out->n_values) return fail(DMB_CONFIG, "update body is NULL");
@@ -560,6 +561,8 @@ int encode(dmb_ctx* ctx, DevStatus* st, bool sgd, const float* g, const float* m
     a.body = static_cast<uint8_t*>(out->body);
     a.sgd = sgd_scalars(beta, 0.0);
     a.status = st;
+    a.n_src = n_src;
+    for (int q = 0; q < n_src; ++q) a.g_src[q] = srcs[q];
     if (int rc = attach_fallback(ctx, &a)) return rc;
     if (mask_layout(ctx, cfg, len)) {
       if (!tc3_supported(sgd ? ChunkMode::EncodeSgd : ChunkMode::EncodeAdam, a))
@@ -824,6 +827,22 @@ int dmb_demo_sgd_prepare(dmb_ctx* ctx, const float* grad, const float* m_in, flo
   return DMB_OK;
 }
 
+int dmb_demo_sgd_prepare_members(dmb_ctx* ctx, const float* const* members, uint32_t n_members, float* grad_mean,
+                                 const float* m_in, float* m_out, uint64_t len, const dmb_opt_cfg* opt,
+                                 const dmb_rep_cfg* cfg, uint64_t step, uint32_t shard, dmb_update* out,
+                                 void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (!members || n_members == 0 || n_members > (uint32_t)kMaxReplicas)
+    return fail(DMB_PROTOCOL, "reduce-scatter over %u members", n_members);
+  if (cfg->scheme != DMB_DEMO || n_members > 2) {  // the mean first, then the prepare
+    if (len) launch_grad_mean(members, (int)n_members, len, grad_mean, s);
+    return dmb_demo_sgd_prepare(ctx, grad_mean, m_in, m_out, len, opt, cfg, step, shard, out, nullptr, nullptr,
+                                stream);
+  }
+  return encode(ctx, ctx->status, true, grad_mean, m_in, m_out, opt->momentum_decay, len, cfg, step, shard, out,
+                nullptr, nullptr, s, members, (int)n_members);
+}
+
 int dmb_demo_sgd_apply(dmb_ctx* ctx, float* params, const float* q, uint64_t n, double lr,
                        void* stream) {
   if (!n) return DMB_OK;
@@ -845,6 +864,20 @@ int dmb_adamw_prepare(dmb_ctx* ctx, const float* grad, uint64_t len, const dmb_r
     return last_launch();
   }
   return DMB_OK;
+}
+
+int dmb_adamw_prepare_members(dmb_ctx* ctx, const float* const* members, uint32_t n_members, float* grad_mean,
+                              uint64_t len, const dmb_rep_cfg* cfg, uint64_t step, uint32_t shard,
+                              dmb_update* out, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (!members || n_members == 0 || n_members > (uint32_t)kMaxReplicas)
+    return fail(DMB_PROTOCOL, "reduce-scatter over %u members", n_members);
+  if (cfg->scheme != DMB_DEMO || n_members > (uint32_t)kMaxGradSrc) {  // the mean first, then the prepare
+    if (len) launch_grad_mean(members, (int)n_members, len, grad_mean, s);
+    return dmb_adamw_prepare(ctx, grad_mean, len, cfg, step, shard, out, nullptr, stream);
+  }
+  return encode(ctx, ctx->status, false, grad_mean, nullptr, nullptr, 0.0, len, cfg, step, shard, out, nullptr,
+                nullptr, s, members, (int)n_members);
 }
 
 int dmb_adamw_apply(dmb_ctx* ctx, float* params, float* exp_avg, float* exp_avg_sq,
@@ -1031,6 +1064,43 @@ int dmb_step_sgd_local(dmb_ctx* ctx, const float* grad, const float* m_in, float
   return fail(DMB_CONFIG, "the fused one-member step covers the demo scheme; use prepare + merge_apply");
 }
 
+int dmb_step_sgd_local_members(dmb_ctx* ctx, const float* const* members, uint32_t n_members, float* grad_mean,
+                               const float* m_in, float* m_out, const float* p_in, float* p_out, uint64_t len,
+                               const dmb_opt_cfg* opt, const dmb_rep_cfg* cfg, uint64_t step, uint32_t shard,
+                               double lr, dmb_update* out, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (!members || n_members == 0 || n_members > (uint32_t)kMaxReplicas)
+    return fail(DMB_PROTOCOL, "reduce-scatter over %u members", n_members);
+  if (n_members > 2 || cfg->scheme != DMB_DEMO) {
+    if (len) launch_grad_mean(members, (int)n_members, len, grad_mean, s);
+    return dmb_step_sgd_local(ctx, grad_mean, m_in, m_out, p_in, p_out, len, opt, cfg, step, shard, lr, out, stream);
+  }
+  dmb_update hdr{};
+  if (out) hdr.body = out->body;
+  if (int rc = plan(cfg, len, step, shard, &hdr)) return rc;
+  if (out) *out = hdr;
+  if (!len) return DMB_OK;
+  if (out && out->body) {
+    if (int rc = prep_values_region(out, cfg->transfer_dtype, s)) return rc;
+  }
+  ChunkArgs a{};
+  a.geo = geometry(cfg, len);
+  if (int rc = get_basis(ctx, a.geo.s, &a.basis)) return rc;
+  a.g = grad_mean;
+  a.n_src = (int)n_members;
+  for (uint32_t q = 0; q < n_members; ++q) a.g_src[q] = members[q];
+  a.m_in = m_in;
+  a.m_out = m_out;
+  a.p_in = p_in;
+  a.p_out = p_out;
+  a.body = out ? static_cast<uint8_t*>(out->body) : nullptr;
+  a.sgd = sgd_scalars(opt->momentum_decay, lr);
+  a.status = ctx->status;
+  if (int rc = attach_fallback(ctx, &a)) return rc;
+  launch_chunk_kernel(ChunkMode::StepSgd, a, s);
+  return last_launch();
+}
+
 int dmb_step_adamw_local(dmb_ctx* ctx, const float* grad, const float* p_in, float* p_out,
                          const float* ea_in, float* ea_out, const float* es_in, float* es_out,
                          uint64_t* steps, uint64_t len, const dmb_opt_cfg* opt,
@@ -1052,6 +1122,50 @@ int dmb_step_adamw_local(dmb_ctx* ctx, const float* grad, const float* p_in, flo
   a.geo = geometry(cfg, len);
   if (int rc = get_basis(ctx, a.geo.s, &a.basis)) return rc;
   a.g = grad;
+  a.p_in = p_in;
+  a.p_out = p_out;
+  a.ea_in = ea_in;
+  a.ea_out = ea_out;
+  a.es_in = es_in;
+  a.es_out = es_out;
+  a.body = out ? static_cast<uint8_t*>(out->body) : nullptr;
+  a.adam = adam_scalars(opt, *steps, lr);
+  a.status = ctx->status;
+  if (int rc = attach_fallback(ctx, &a)) return rc;
+  launch_chunk_kernel(ChunkMode::StepAdam, a, s);
+  return last_launch();
+}
+
+int dmb_step_adamw_local_members(dmb_ctx* ctx, const float* const* members, uint32_t n_members, float* grad_mean,
+                                 const float* p_in, float* p_out, const float* ea_in, float* ea_out,
+                                 const float* es_in, float* es_out, uint64_t* steps, uint64_t len,
+                                 const dmb_opt_cfg* opt, const dmb_rep_cfg* cfg, uint64_t step, uint32_t shard,
+                                 double lr, dmb_update* out, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (!members || n_members == 0 || n_members > (uint32_t)kMaxReplicas)
+    return fail(DMB_PROTOCOL, "reduce-scatter over %u members", n_members);
+  if (n_members > 2) {  // the fused load takes two members next to the state staging
+    if (len) launch_grad_mean(members, (int)n_members, len, grad_mean, s);
+    return dmb_step_adamw_local(ctx, grad_mean, p_in, p_out, ea_in, ea_out, es_in, es_out, steps, len, opt, cfg,
+                                step, shard, lr, out, stream);
+  }
+  dmb_update hdr{};
+  if (out) hdr.body = out->body;
+  if (int rc = plan(cfg, len, step, shard, &hdr)) return rc;
+  if (out) *out = hdr;
+  if (cfg->scheme != DMB_DEMO)
+    return fail(DMB_CONFIG, "the fused one-member step covers the demo scheme; use prepare + merge_apply");
+  *steps += 1;
+  if (!len) return DMB_OK;
+  if (out && out->body) {
+    if (int rc = prep_values_region(out, cfg->transfer_dtype, s)) return rc;
+  }
+  ChunkArgs a{};
+  a.geo = geometry(cfg, len);
+  if (int rc = get_basis(ctx, a.geo.s, &a.basis)) return rc;
+  a.g = grad_mean;
+  a.n_src = (int)n_members;
+  for (uint32_t q = 0; q < n_members; ++q) a.g_src[q] = members[q];
   a.p_in = p_in;
   a.p_out = p_out;
   a.ea_in = ea_in;

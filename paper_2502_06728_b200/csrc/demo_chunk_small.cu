@@ -20,6 +20,19 @@ static bool force_fp64_env() {
 void launch_chunk_kernel(ChunkMode mode, const ChunkArgs& a_in, cudaStream_t stream) {
   ChunkArgs a = a_in;
   if (force_fp64_env()) a.force_fp64 = 1;
+  if (a.n_src > 0) {
+    // the shard group's reduce-scatter fused into the gradient load: the tensor-core kernel
+    // averages the members' tiles and writes the mean to a.g; the partial last chunk's mean
+    // comes first (its SIMT pass reads a.g).  Anywhere else the mean is a pass of its own.
+    const bool fused = tc_enabled() && a.fb_list && a.fb_count && tc3_supported(mode, a);
+    const uint64_t from = fused ? (a.geo.len / a.geo.s) * a.geo.s : 0;
+    if (from < a.geo.len) {
+      const float* tails[kMaxGradSrc];
+      for (int q = 0; q < a.n_src; ++q) tails[q] = a.g_src[q] + from;
+      launch_grad_mean(tails, a.n_src, a.geo.len - from, const_cast<float*>(a.g) + from, stream);
+    }
+    if (!fused) a.n_src = 0;
+  }
   if (tc_enabled() && a.fb_list && a.fb_count && tc3_supported(mode, a)) {
     // warp-specialised tensor-core kernel; the chunks its FP32 bound cannot certify are
     // re-derived exactly by the FP64 fix-up kernel; a partial last chunk (its own

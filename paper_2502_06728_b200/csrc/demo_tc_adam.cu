@@ -527,13 +527,31 @@ __device__ __forceinline__ uint32_t mask_ge(const float (&c)[16], float T) {
 
 struct TensorMaps {
   CUtensorMap g, p_in, ea_in, es_in, p_out, ea_out, es_out;
+  CUtensorMap gs[kMaxGradSrc];  // member gradients of a fused reduce-scatter (a.n_src > 0)
 };
+// gradient stage slots of a fused reduce-scatter: member q lands in src_slot<MODE>(q).  AdamW:
+// the scratch, then (EncodeAdam, no state) staging tiles 0-1, so StepAdam takes two members and
+// EncodeAdam four; the SGD modes keep the momentum tile in the scratch and take two, the second
+// in a free staging tile (EncodeSgd: 0, StepSgd: 2)
+template <ChunkMode MODE>
+__host__ __device__ constexpr uint32_t src_slot(int q) {
+  return q == 0 ? OFF_G
+                : (MODE == ChunkMode::EncodeSgd ? OFF_ST
+                   : MODE == ChunkMode::StepSgd ? OFF_ST + 2 * TILE
+                                                : (q == 1 ? OFF_SCR : (q == 2 ? OFF_ST : OFF_ST + TILE)));
+}
+__host__ __device__ constexpr int max_src(ChunkMode m) {
+  return m == ChunkMode::EncodeAdam ? kMaxGradSrc
+                                    : (m == ChunkMode::StepAdam || m == ChunkMode::StepSgd || m == ChunkMode::EncodeSgd) ? 2 : 0;
+}
 
 template <ChunkMode MODE, int WIRE>
 __global__ void __maxnreg__(128)
     demo_tc_adam_kernel(const ChunkArgs a, const __grid_constant__ TensorMaps maps) {
   constexpr bool kEncodeOnly = MODE == ChunkMode::EncodeAdam;  // no state at all
   constexpr bool kMergeSgd = MODE == ChunkMode::MergeSgd;      // no forward DCT, no gradient
+  // modes that can take the shard group's member gradients directly (a.n_src > 0)
+  constexpr bool kSrcModes = max_src(MODE) > 0;
   constexpr bool kMerge = MODE == ChunkMode::MergeAdam || kMergeSgd;
   constexpr bool kSgd = MODE == ChunkMode::StepSgd;  // m = beta m + g; m -= local_q; p -= lr Q
   constexpr bool kEncSgd = MODE == ChunkMode::EncodeSgd;  // m = beta m + g; m -= local_q; payload
@@ -634,6 +652,18 @@ __global__ void __maxnreg__(128)
   // gradient tile t (and, SGD modes, the momentum tile) into the single gradient stage: issued
   // by one thread of the apply warps once the front of the previous tile has consumed it
   auto load_grad = [&](uint64_t t) {
+    if (kSrcModes && a.n_src > 0) {  // every member's tile of the fused reduce-scatter
+      mbar_arrive_expect_tx(bar_g, (uint32_t)(a.n_src + (kMomentum ? 1 : 0)) * TILE);
+      for (int q = 0; q < a.n_src; ++q) {
+        tma_2d(smem + src_slot<MODE>(q), &maps.gs[q], 0, (int)(t * TM), bar_g);
+        tma_2d(smem + src_slot<MODE>(q) + BOX, &maps.gs[q], 32, (int)(t * TM), bar_g);
+      }
+      if (kMomentum) {
+        tma_2d(smem + OFF_M, &maps.ea_in, 0, (int)(t * TM), bar_g);
+        tma_2d(smem + OFF_M + BOX, &maps.ea_in, 32, (int)(t * TM), bar_g);
+      }
+      return;
+    }
     mbar_arrive_expect_tx(bar_g, kMomentum ? 2 * TILE : TILE);
     tma_2d(smem + OFF_G, &maps.g, 0, (int)(t * TM), bar_g);
     tma_2d(smem + OFF_G + BOX, &maps.g, 32, (int)(t * TM), bar_g);
@@ -767,6 +797,30 @@ __global__ void __maxnreg__(128)
           x[4 * e + 2] = v.z;
           x[4 * e + 3] = v.w;
         }
+        if (kSrcModes && a.n_src > 0 && part != kRing) {
+          // the member-order mean (mean_of, vec.cpp:18-26: from 0, members in order, then / n),
+          // written back in place so the gradient stage is stored to g as the shard's mean
+          const int ns = a.n_src;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) x[e] = __fadd_rn(0.0f, x[e]);
+          for (int q = 1; q < ns; ++q) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float4 v = *reinterpret_cast<const float4*>(smem + src_slot<MODE>(q) + sw_off(trow, 4 * h + e));
+              x[4 * e] = __fadd_rn(x[4 * e], v.x);
+              x[4 * e + 1] = __fadd_rn(x[4 * e + 1], v.y);
+              x[4 * e + 2] = __fadd_rn(x[4 * e + 2], v.z);
+              x[4 * e + 3] = __fadd_rn(x[4 * e + 3], v.w);
+            }
+          }
+          const float fn = (float)ns;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) x[e] = __fdiv_rn(x[e], fn);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            *reinterpret_cast<float4*>(smem + OFF_G + sw_off(trow, 4 * h + e)) =
+                make_float4(x[4 * e], x[4 * e + 1], x[4 * e + 2], x[4 * e + 3]);
+        }
         if (part != kRing) {
 #pragma unroll
           for (int e = 0; e < 16; ++e) fin = fin && isfinite(x[e]);
@@ -824,7 +878,16 @@ __global__ void __maxnreg__(128)
     // done with the current one
     const bool lead = tid == 32 * kSelWarps;
     auto next_grad = [&](uint64_t t) {
+      const bool wb = kSrcModes && a.n_src > 0;
+      if (wb) fence_proxy_async_smem();  // the mean written into the stage, for the TMA store
       named_sync(1, kAppWarps * 32);
+      if (wb && lead && t >= G && t - G < ntiles) {
+        // the mean of the tile just consumed (t - G) to g, read out before the stage refills
+        tma_2d_store(&maps.g, 0, (int)((t - G) * TM), smem + OFF_G);
+        tma_2d_store(&maps.g, 32, (int)((t - G) * TM), smem + OFF_G + BOX);
+        bulk_commit();
+        bulk_wait_read();
+      }
       if (lead && t < ntiles) load_grad(t);
     };
     // MASK_SIGN payload of tile t (pay_off): row trow's mask and code words from the quad's
@@ -994,6 +1057,7 @@ __global__ void __maxnreg__(128)
         if (pay_off) payload(tile, it);
       }
     }
+    if (kSrcModes && a.n_src > 0 && lead) bulk_wait_all();  // the last means are in g
     goto teardown;
   }
 
@@ -1253,20 +1317,32 @@ __global__ void __maxnreg__(128)
             if (act0 && !def0) cw[4 * r0 + s] = code_word(sel0, sg0);
             if (act1 && !def1) cw[4 * r1 + s] = code_word(sel1, sg1);
           }
+          // values in ascending frequency: the value number of column 8r + 2s + b is the rank byte r
+          // of the chunk mask (SWAR, pair_ranks) plus b * the selection bit of 8r + 2s; the stores
+          // specialised per value type so they predicate instead of branching
+          auto put_row = [&](uint32_t sel, uint64_t all, uint64_t row, const float (&cv)[16], auto st) {
+            const uint64_t rk = pair_ranks(all, s);
+            const uint64_t base = row * (uint64_t)k;
 #pragma unroll
-          for (int e = 0; e < 16 && !words; ++e) {
-            const int col = qcol(e, s);
-            const uint64_t below = (1ull << col) - 1ull;
-            if (act0 && !def0 && ((sel0 >> e) & 1u)) {
-              const uint64_t t = r0 * (uint64_t)k + __popcll(all0 & below);
-              if (!mask_wire) idx[t] = (uint32_t)col;
-              store_wire_value(vals, t, cond_w<WIRE>(c0[e]), vd);
+            for (int e = 0; e < 16; ++e) {
+              const uint32_t n = ((uint32_t)(rk >> (8 * (e >> 1))) & 0xffu) + ((e & 1) ? (sel >> (e - 1)) & 1u : 0u);
+              if ((sel >> e) & 1u) {
+                if (!mask_wire) idx[base + n] = (uint32_t)qcol(e, s);
+                st(base + n, cond_w<WIRE>(cv[e]));
+              }
             }
-            if (act1 && !def1 && ((sel1 >> e) & 1u)) {
-              const uint64_t t = r1 * (uint64_t)k + __popcll(all1 & below);
-              if (!mask_wire) idx[t] = (uint32_t)col;
-              store_wire_value(vals, t, cond_w<WIRE>(c1[e]), vd);
-            }
+          };
+          auto put = [&](auto st) {
+            if (act0 && !def0) put_row(sel0, all0, r0, c0, st);
+            if (act1 && !def1) put_row(sel1, all1, r1, c1, st);
+          };
+          if (!words) {
+            if (vd == DMB_FP32)
+              put([&](uint64_t t, float w) { reinterpret_cast<float*>(vals)[t] = w; });
+            else if (vd == DMB_FP16)
+              put([&](uint64_t t, float w) { reinterpret_cast<__half*>(vals)[t] = __float2half_rn(w); });
+            else
+              put([&](uint64_t t, float w) { store_wire_value(vals, t, w, vd); });
           }
         }
       } else {
@@ -1912,6 +1988,11 @@ bool tc3_supported(ChunkMode mode, const ChunkArgs& a) {
     return false;
   if (mode == ChunkMode::MergeAdam && (a.own_rank < 0 || a.own_rank >= a.in.R)) return false;
   auto al = [](const void* p) { return p && (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  if (a.n_src > 0) {  // fused reduce-scatter: up to max_src members
+    if (a.n_src > max_src(mode)) return false;
+    for (int q = 0; q < a.n_src; ++q)
+      if (!al(a.g_src[q])) return false;
+  }
   switch (mode) {
     case ChunkMode::EncodeAdam: return al(a.g);
     case ChunkMode::EncodeSgd: return al(a.g) && al(a.m_in) && al(a.m_out);
@@ -1930,6 +2011,7 @@ void launch_tc3_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream) 
   memset(&maps, 0, sizeof(maps));
   const uint64_t rows = a.geo.len / S;
   if (mode != ChunkMode::MergeSgd) tile_map(&maps.g, a.g, rows);
+  for (int q = 0; q < a.n_src; ++q) tile_map(&maps.gs[q], a.g_src[q], rows);
   if (mode == ChunkMode::StepSgd || mode == ChunkMode::EncodeSgd) {
     // the split reads g and m (ea_in); staging: p in / out (StepSgd), m out
     tile_map(&maps.ea_in, a.m_in, rows);

@@ -173,7 +173,13 @@ struct ChunkArgs {
   int force_fp64;
   uint64_t first_chunk;     // SIMT kernel, non-list mode: start at this chunk (tail fix-up)
   unsigned long long* dbg;  // optional event timestamps (tests / tuning only)
+  // the shard group's reduce-scatter fused into the gradient load (StepAdam / EncodeAdam on the
+  // tensor-core kernel): the encoded gradient is the member-order mean of g_src[0..n_src), and
+  // the kernel writes that mean to g (which every later reader -- fix-up, tail, merge -- uses)
+  const float* g_src[4];
+  int n_src;
 };
+constexpr int kMaxGradSrc = 4;
 
 // Dispatch: tensor-core kernel + FP64 fix-up for s == 64 when enabled, else SIMT.
 void launch_chunk_kernel(ChunkMode mode, const ChunkArgs& a, cudaStream_t stream);
