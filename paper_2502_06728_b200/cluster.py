@@ -784,11 +784,15 @@ class HybridCluster:
         off0 = self.accel * self.spec.extent
         spans = [(b["lo"], b["hi"]) for b in self.buckets] or [(0, self.spec.real_len)]
         copied = []
-        direct = os.environ.get("DMB_PULL_DIRECT") == "1" and self.rep.scheme == Scheme.DeMo
+        # the fused path reads the peers' slices with the step kernel's own TMA over NVLink (no
+        # staging: measured 2x1 AdamW 5.6 ms against 6.6 ms staged by the copy engines);
+        # DMB_PULL_STAGED=1 stages them anyway
+        direct = (os.environ.get("DMB_PULL_STAGED") != "1" and self.rep.scheme == Scheme.DeMo and not self.sgd
+                  and A <= (2 if self.fused else 4))
         with torch.cuda.stream(self._copy_stream):
             hdl.barrier(channel=1)  # every member's gradient of this step is written
             for lo, hi in spans:
-                if direct:  # (experiment) the kernel's TMA reads the peers' slices over NVLink itself
+                if direct:
                     break
                 for a, stg in self._gstage.items():
                     stg[lo:hi].copy_(views[a][off0 + lo:off0 + hi], non_blocking=True)
@@ -804,8 +808,10 @@ class HybridCluster:
             ev = torch.cuda.Event()
             ev.record(self._copy_stream)
             copied = [ev] * len(spans)
-        self._pull_fused = (self.rep.scheme == Scheme.DeMo
-                            and A <= (4 if not (self.sgd or self.fused) else 2)
+        # DeMo-SGD keeps the mean as a pass of its own: its front is busier (the momentum tile) and
+        # the fused SGD load measured slower at 2x1 (7.3 ms against 6.3 ms)
+        self._pull_fused = (self.rep.scheme == Scheme.DeMo and not self.sgd
+                            and A <= (2 if self.fused else 4)
                             and all(t.data_ptr() % 16 == 0 and (4 * b["lo"]) % 16 == 0
                                     for t in srcs for b in (self.buckets or [dict(lo=0)])))
         if self._pull_fused:
