@@ -784,11 +784,12 @@ class HybridCluster:
         off0 = self.accel * self.spec.extent
         spans = [(b["lo"], b["hi"]) for b in self.buckets] or [(0, self.spec.real_len)]
         copied = []
-        # the fused path reads the peers' slices with the step kernel's own TMA over NVLink (no
-        # staging: measured 2x1 AdamW 5.6 ms against 6.6 ms staged by the copy engines);
-        # DMB_PULL_STAGED=1 stages them anyway
-        direct = (os.environ.get("DMB_PULL_STAGED") != "1" and self.rep.scheme == Scheme.DeMo and not self.sgd
-                  and A <= (2 if self.fused else 4))
+        # the one-pass R = 1 step reads the peers' slices with its own TMA over NVLink (2x1 AdamW:
+        # 5.7 ms, against 6.6 ms staged by the copy engines); the R > 1 prepare is faster on staged
+        # slices (2x2 AdamW: 8.2 ms staged, 9.1 ms direct), its exchange sharing the links
+        direct = (self.fused and os.environ.get("DMB_PULL_STAGED") != "1"
+                  and os.environ.get("DMB_PULL_FUSED", "1") != "0"
+                  and self.rep.scheme == Scheme.DeMo and not self.sgd and A <= 2)
         with torch.cuda.stream(self._copy_stream):
             hdl.barrier(channel=1)  # every member's gradient of this step is written
             for lo, hi in spans:
@@ -810,8 +811,8 @@ class HybridCluster:
             copied = [ev] * len(spans)
         # DeMo-SGD keeps the mean as a pass of its own: its front is busier (the momentum tile) and
         # the fused SGD load measured slower at 2x1 (7.3 ms against 6.3 ms)
-        self._pull_fused = (self.rep.scheme == Scheme.DeMo and not self.sgd
-                            and A <= (2 if self.fused else 4)
+        self._pull_fused = (os.environ.get("DMB_PULL_FUSED", "1") != "0" and self.rep.scheme == Scheme.DeMo
+                            and not self.sgd and A <= (2 if self.fused else 4)
                             and all(t.data_ptr() % 16 == 0 and (4 * b["lo"]) % 16 == 0
                                     for t in srcs for b in (self.buckets or [dict(lo=0)])))
         if self._pull_fused:
