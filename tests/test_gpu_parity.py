@@ -704,3 +704,49 @@ def test_tc_step_few_tiles_per_cta(oracle, tiles_per_cta, k):
     chunk_close(host(ead), ew, 64, what="exp_avg")
     chunk_close(host(esd), sw, 64, what="exp_avg_sq")
     update_close(host(pd), pw, p0, 1e-3, 64)
+
+
+@pytest.mark.parametrize("opt_kind,sign", [("sgd", True), ("sgd", False), ("adamw", True)])
+def test_v2_near_ties_and_single_frequency(oracle, monkeypatch, opt_kind, sign):
+    """The paths with inspection outputs (local_q / m_accum) run the 16-warp v2 tensor-core
+    kernel (demo_tc.cu) with its own derived radius: chunks built with the k-th and (k+1)-th |c|
+    a relative 1e-3 .. 1e-7 apart, and chunks with a single nonzero frequency, must select the
+    oracle's indices bit-exactly (near ties deferred to the FP64 fix-up) with local_q and m_accum
+    within the 1e-5 bar."""
+    p = P()
+    monkeypatch.setenv("DMB_TC", "1")
+    S, k, nch = 64, 8, 128 * 4
+    rng = np.random.default_rng(808)
+    j = np.arange(S)
+    B = np.sqrt(2.0 / S) * np.cos(np.pi * (2 * j[None, :] + 1) * j[:, None] / (2 * S))
+    B[0] /= np.sqrt(2.0)
+    c = rng.standard_normal((nch, S)) * 1e-3
+    gaps = np.array([1e-3, 1e-4, 3e-5, 1e-7])[np.arange(nch) % 4]
+    for r in range(nch):
+        if r % 16 == 5:  # a single frequency: one nonzero coefficient, the rest exact zeros (ties)
+            c[r] = 0.0
+            c[r, (r * 7) % S] = 2e-3
+            continue
+        order = np.argsort(-np.abs(c[r]))
+        kth, nxt = order[k - 1], order[k]
+        c[r, nxt] = np.sign(c[r, nxt]) * abs(c[r, kth]) * (1.0 - gaps[r])
+    g = (c @ B).astype(np.float32).reshape(-1)
+    n = g.size
+    rep = Rep(scheme=DEMO, chunk_size=S, top_k=k, compression=k / S, sign_mode=sign, seed=1234)
+    cfg = rep_to_cfg(rep)
+    if opt_kind == "sgd":
+        st = p.MomentumState.make(p.OptimizerKind.DemoSgd, n)  # zero momentum: m_acc = g
+        tr = p.StepTrace()
+        enc = p.demo_sgd_prepare(st, dev(g), p.OptimizerConfig(momentum_decay=0.9), cfg, 2, 0, tr)
+        chunk_close(host(tr.m_accum), g.astype(np.float64), 64, what="m_accum")
+        local_q = host(tr.local_q)
+    else:
+        enc = p.adamw_prepare(dev(g), cfg, 2, 0)
+        local_q = host(enc.local_q)
+    want = oracle.select_and_encode(g.astype(np.float64), rep, 2, 0)
+    assert np.array_equal(enc.update.freq_indices.cpu().numpy().astype(np.uint32), want["freq_indices"])
+    if sign:
+        assert np.array_equal(host(enc.update.values), want["values"])
+    else:  # FP32 coefficients against the oracle's FP64 ones, per chunk (k values each)
+        chunk_close(host(enc.update.values), want["values"], k, what="values")
+    chunk_close(local_q, want["local_q"], 64, what="local_q")
