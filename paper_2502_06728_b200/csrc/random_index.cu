@@ -107,44 +107,54 @@ __device__ __forceinline__ uint32_t lemire(uint64_t x, uint64_t n, bool& rejecte
 // CTA's barriers).  Substream b: window P_b(T) s0 by correlation, then W / 312 twists on
 // ping-pong windows (two barriers per twist); draw d = output o (no rejection before o
 // assumed; the first output that could be one is reported in *reject)
-constexpr int kSubPerCta = 2;
-constexpr int kBlockThreads = kSubPerCta * kMtThreads;
+constexpr int kSubPerCta = 1;
+constexpr int kCorrGroups = 2;  // thread groups sharing one substream's correlation
+constexpr int kBlockThreads = kCorrGroups * kMtThreads;
+constexpr uint16_t kZeroPos = (uint16_t)kMtSeqWords;  // a term list's padding: words past the sequence, zero
 
 __global__ void __launch_bounds__(kBlockThreads) mt_block_kernel(const uint64_t* __restrict__ seq,
-                                                                 const uint64_t* __restrict__ polys, uint64_t W,
+                                                                 const uint16_t* __restrict__ pos,
+                                                                 const uint32_t* __restrict__ pos_off, uint64_t W,
                                                                  uint64_t nsub, uint64_t len, uint64_t ndraws,
                                                                  uint32_t* __restrict__ draws,
                                                                  uint64_t* __restrict__ windows,
                                                                  unsigned long long* __restrict__ reject) {
   extern __shared__ uint64_t sm[];
-  uint64_t* xs = sm;                               // the engine's first kMtSeqWords words
-  uint64_t* poly = xs + kMtSeqWords;               // [sub][312]: P_b, bit i = coefficient of x^i
-  uint64_t* win = poly + kSubPerCta * kMtN;        // [sub][2][312]: ping-pong windows
-  const int sub = threadIdx.x / kMtThreads, t = threadIdx.x % kMtThreads;
-  const uint64_t b = (uint64_t)blockIdx.x * kSubPerCta + sub;
-  const bool live = b < nsub && t < kMtN;
+  uint64_t* xs = sm;                               // the engine's first kMtSeqWords words, then kMtN zeros
+  uint64_t* win = xs + kMtSeqWords + kMtN;         // [2][312]: ping-pong windows
+  uint64_t* part = win + 2 * kMtN;                 // [312]: the second group's half of the correlation
+  const int grp = threadIdx.x / kMtThreads, t = threadIdx.x % kMtThreads;
+  const uint64_t b = blockIdx.x;
+  const bool live = b < nsub && t < kMtN && grp == 0;
   for (uint64_t i = threadIdx.x; i < kMtSeqWords; i += kBlockThreads) xs[i] = seq[i];
-  if (live) poly[sub * kMtN + t] = b ? polys[b * kMtN + t] : 0ull;
+  for (int i = threadIdx.x; i < kMtN; i += kBlockThreads) xs[kMtSeqWords + i] = 0ull;
   __syncthreads();
-  uint64_t* w0 = win + sub * 2 * kMtN;
-  if (live) {
-    uint64_t acc = 0;
-    if (b == 0) {
-      acc = xs[t];
-    } else {
-      const uint32_t* p32 = reinterpret_cast<const uint32_t*>(poly + sub * kMtN);
-      const uint64_t* xt = xs + t;
-      for (int w = 0; w < 2 * kMtN; ++w, xt += 32) {  // uniform within a substream
-        uint32_t bits = p32[w];
-        while (bits) {
-          const int i = __ffs(bits) - 1;
-          bits &= bits - 1;
-          acc ^= xt[i];
-        }
-      }
+  uint64_t* w0 = win;
+  uint64_t acc = 0;
+  if (b < nsub && t < kMtN) {
+    // the correlation: word t of the window = XOR over the exponents i of P_b's terms of the
+    // engine word t + i.  The exponents come as a list (16 bits each, four per load; the last
+    // group padded with kZeroPos, which reads zeros), four independent accumulators keep four
+    // loads in flight, the two thread groups take alternate groups of four terms
+    const uint64_t* pq = reinterpret_cast<const uint64_t*>(pos + pos_off[b]);
+    const uint32_t nq = (pos_off[b + 1] - pos_off[b]) / 4;
+    const uint64_t* xt = xs + t;
+    uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    for (uint32_t q = grp; q < nq; q += kCorrGroups) {  // uniform within a group: broadcast loads
+      const uint64_t w = __ldg(pq + q);
+      a0 ^= xt[(uint32_t)(w & 0xffffu)];
+      a1 ^= xt[(uint32_t)((w >> 16) & 0xffffu)];
+      a2 ^= xt[(uint32_t)((w >> 32) & 0xffffu)];
+      a3 ^= xt[(uint32_t)(w >> 48)];
     }
-    w0[t] = acc;
-    windows[b * kMtN + t] = acc;
+    acc = (a0 ^ a1) ^ (a2 ^ a3);
+    if (grp) part[t] = acc;
+  }
+  __syncthreads();
+  if (live) {
+    const uint64_t win0 = acc ^ part[t];
+    w0[t] = win0;
+    windows[b * kMtN + t] = win0;
   }
   const uint64_t twists = W / kMtN;
   const uint64_t o0 = b * W;
@@ -152,10 +162,10 @@ __global__ void __launch_bounds__(kBlockThreads) mt_block_kernel(const uint64_t*
     const uint64_t* cur = w0 + (tw & 1) * kMtN;
     uint64_t* nxt = w0 + ((tw + 1) & 1) * kMtN;
     __syncthreads();  // cur complete (previous twist or the correlation)
-    if (t < 156) nxt[t] = twist_word(cur[t], cur[t + 1], cur[t + 156]);
+    if (grp == 0 && t < 156) nxt[t] = twist_word(cur[t], cur[t + 1], cur[t + 156]);
     __syncthreads();
-    if (t >= 156 && t < 311) nxt[t] = twist_word(cur[t], cur[t + 1], nxt[t - 156]);
-    if (t == 311) nxt[311] = twist_word(cur[311], nxt[0], nxt[155]);
+    if (grp == 0 && t >= 156 && t < 311) nxt[t] = twist_word(cur[t], cur[t + 1], nxt[t - 156]);
+    if (grp == 0 && t == 311) nxt[311] = twist_word(cur[311], nxt[0], nxt[155]);
     __syncthreads();
     const uint64_t o = o0 + tw * kMtN + t;
     if (live && o < ndraws) {
@@ -207,9 +217,14 @@ __global__ void __launch_bounds__(kMtThreads) mt_fixup_kernel(const uint64_t* __
 constexpr int kDeg = 19937;
 constexpr int kPW = kMtN;  // words of a reduced polynomial (degree < 19937)
 
+struct DevPositions {
+  uint16_t* pos = nullptr;      // the exponents of every P_b's terms, groups of four (kZeroPos pad)
+  uint32_t* off = nullptr;      // [b]: start of P_b's list in pos; [blocks]: the end
+  uint64_t blocks = 0;
+};
 struct JumpSet {
-  std::vector<std::vector<uint64_t>> polys;           // x^(b W) mod phi, b = 0, 1, ...
-  std::map<int, std::pair<uint64_t*, uint64_t>> dev;  // device copies (pointer, polys held)
+  std::vector<std::vector<uint64_t>> polys;  // x^(b W) mod phi, b = 0, 1, ...
+  std::map<int, DevPositions> dev;           // device copies (term lists)
 };
 struct JumpTable {
   std::mutex mu;
@@ -374,7 +389,7 @@ void start_set(JumpTable& J, uint64_t W, JumpSet& S) {
 
 // the jump polynomials of substreams 0 .. blocks-1 of length W on `device` (host work once per
 // process and W)
-const uint64_t* jump_polys(uint64_t W, uint64_t blocks, int device, const char** err) {
+const DevPositions* jump_polys(uint64_t W, uint64_t blocks, int device, const char** err) {
   JumpTable& J = jump_table();
   std::lock_guard<std::mutex> lock(J.mu);
   if (!J.ready) {
@@ -406,18 +421,28 @@ const uint64_t* jump_polys(uint64_t W, uint64_t blocks, int device, const char**
     for (auto& x : th) x.join();
   }
   auto& d = S.dev[device];
-  if (d.second < blocks) {  // the old copy is kept: kernels in flight may still read it
-    uint64_t* p = nullptr;
-    if (cudaMalloc(&p, blocks * kPW * 8) != cudaSuccess) {
+  if (d.blocks < blocks) {  // the old copy is kept: kernels in flight may still read it
+    std::vector<uint16_t> pos;
+    std::vector<uint32_t> off(blocks + 1);
+    for (uint64_t b = 0; b < blocks; ++b) {
+      off[b] = (uint32_t)pos.size();
+      const std::vector<uint64_t>& P = S.polys[b];
+      for (int i = 0; i < kDeg; ++i)
+        if ((P[i >> 6] >> (i & 63)) & 1u) pos.push_back((uint16_t)i);
+      while ((pos.size() - off[b]) % 4) pos.push_back(kZeroPos);
+    }
+    off[blocks] = (uint32_t)pos.size();
+    DevPositions nd;
+    if (cudaMalloc(&nd.pos, pos.size() * 2 + 8) != cudaSuccess || cudaMalloc(&nd.off, off.size() * 4) != cudaSuccess) {
       *err = "cudaMalloc of the jump polynomials failed";
       return nullptr;
     }
-    std::vector<uint64_t> flat(blocks * kPW);
-    for (uint64_t b = 0; b < blocks; ++b) std::memcpy(&flat[b * kPW], S.polys[b].data(), kPW * 8);
-    cudaMemcpy(p, flat.data(), flat.size() * 8, cudaMemcpyHostToDevice);
-    d = {p, blocks};
+    cudaMemcpy(nd.pos, pos.data(), pos.size() * 2, cudaMemcpyHostToDevice);
+    cudaMemcpy(nd.off, off.data(), off.size() * 4, cudaMemcpyHostToDevice);
+    nd.blocks = blocks;
+    d = nd;
   }
-  return d.first;
+  return &d;
 }
 
 __global__ void first_pass(const uint32_t* __restrict__ draws, uint64_t len, uint64_t ndraws,
@@ -622,23 +647,23 @@ int launch_random_indices(uint64_t engine_seed, uint64_t len, uint64_t count, co
       *err = "substream windows scratch too small";
       return DMB_CUDA;
     }
-    const uint64_t* polys = jump_polys(W, nsub, dev, err);
-    if (!polys) return DMB_CUDA;
+    const DevPositions* jp = jump_polys(W, nsub, dev, err);
+    if (!jp) return DMB_CUDA;
     count_launches(9);
     // DMB_MT_FORCE_FIXUP=1 (tests): report a rejection at output 0, so the sequential replay
     // rewrites every draw -- it must reproduce the substreams' draws exactly
     const char* ff = std::getenv("DMB_MT_FORCE_FIXUP");
     cudaMemsetAsync(s.mt_reject, (ff && ff[0] == '1') ? 0x00 : 0xff, sizeof(unsigned long long), stream);
     mt_seq_kernel<<<1, kMtThreads, 0, stream>>>(engine_seed, s.mt_seq);
-    const int smem = (int)((kMtSeqWords + 3 * kSubPerCta * kMtN) * 8);
+    const int smem = (int)((kMtSeqWords + 4 * kMtN) * 8);
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(mt_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr = true;
     }
     const unsigned ctas = (unsigned)((nsub + kSubPerCta - 1) / kSubPerCta);
-    mt_block_kernel<<<ctas, kBlockThreads, smem, stream>>>(s.mt_seq, polys, W, nsub, len, ndraws, s.draws,
-                                                           s.mt_windows, s.mt_reject);
+    mt_block_kernel<<<ctas, kBlockThreads, smem, stream>>>(s.mt_seq, jp->pos, jp->off, W, nsub, len, ndraws,
+                                                           s.draws, s.mt_windows, s.mt_reject);
     mt_fixup_kernel<<<1, kMtThreads, 0, stream>>>(s.mt_windows, W, len, ndraws, s.draws, s.mt_reject);
     cudaMemsetAsync(s.first, 0xff, len * sizeof(uint32_t), stream);
     cudaMemsetAsync(s.second, 0xff, len * sizeof(uint32_t), stream);
