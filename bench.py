@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--sign", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--buckets", type=int, default=8,
+    ap.add_argument("--buckets", type=int, default=4,
                     help="N>1: chunk-aligned buckets of the shard pipelined through prepare / all-gather / merge")
     ap.add_argument("--wire", choices=["mask", "reference"], default="mask",
                     help="N>1 DeMo exchange layout: lossless u64-mask + packed values, or the reference body")
