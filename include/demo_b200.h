@@ -246,8 +246,9 @@ int dmb_grad_mean_pull(dmb_ctx* ctx, const float* const* grads, uint64_t members
  * gradient is the member-order mean of members[0..n) (mean_of, vec.cpp:18-26 -- each a
  * shard-sized slice of a member's gradient, local or staged from a peer), computed in the
  * tensor-core kernel's gradient load and written to grad_mean for the later readers (the merge
- * re-derives local_q from it).  The AdamW prepare takes four members, the other three two;
- * otherwise (and on the generic kernels) the mean is a pass of its own first. */
+ * re-derives local_q from it).  The AdamW prepare takes four members, the one-pass AdamW step
+ * two; otherwise -- more members, the DeMo-SGD entry points, the generic kernels -- the mean is
+ * a pass of its own first (same results). */
 int dmb_adamw_prepare_members(dmb_ctx* ctx, const float* const* members, uint32_t n_members,
                               float* grad_mean, uint64_t len, const dmb_rep_cfg* cfg, uint64_t step,
                               uint32_t shard, dmb_update* out, void* stream);

@@ -834,13 +834,11 @@ int dmb_demo_sgd_prepare_members(dmb_ctx* ctx, const float* const* members, uint
   cudaStream_t s = as_stream(stream);
   if (!members || n_members == 0 || n_members > (uint32_t)kMaxReplicas)
     return fail(DMB_PROTOCOL, "reduce-scatter over %u members", n_members);
-  if (cfg->scheme != DMB_DEMO || n_members > 2) {  // the mean first, then the prepare
-    if (len) launch_grad_mean(members, (int)n_members, len, grad_mean, s);
-    return dmb_demo_sgd_prepare(ctx, grad_mean, m_in, m_out, len, opt, cfg, step, shard, out, nullptr, nullptr,
-                                stream);
-  }
-  return encode(ctx, ctx->status, true, grad_mean, m_in, m_out, opt->momentum_decay, len, cfg, step, shard, out,
-                nullptr, nullptr, s, members, (int)n_members);
+  // the SGD modes take the mean as a pass of its own (their fused load is compiled out: it cost
+  // the one-rank SGD step and measured slower in the cluster), then the prepare
+  if (len) launch_grad_mean(members, (int)n_members, len, grad_mean, s);
+  return dmb_demo_sgd_prepare(ctx, grad_mean, m_in, m_out, len, opt, cfg, step, shard, out, nullptr, nullptr,
+                              stream);
 }
 
 int dmb_demo_sgd_apply(dmb_ctx* ctx, float* params, const float* q, uint64_t n, double lr,
@@ -1071,34 +1069,8 @@ int dmb_step_sgd_local_members(dmb_ctx* ctx, const float* const* members, uint32
   cudaStream_t s = as_stream(stream);
   if (!members || n_members == 0 || n_members > (uint32_t)kMaxReplicas)
     return fail(DMB_PROTOCOL, "reduce-scatter over %u members", n_members);
-  if (n_members > 2 || cfg->scheme != DMB_DEMO) {
-    if (len) launch_grad_mean(members, (int)n_members, len, grad_mean, s);
-    return dmb_step_sgd_local(ctx, grad_mean, m_in, m_out, p_in, p_out, len, opt, cfg, step, shard, lr, out, stream);
-  }
-  dmb_update hdr{};
-  if (out) hdr.body = out->body;
-  if (int rc = plan(cfg, len, step, shard, &hdr)) return rc;
-  if (out) *out = hdr;
-  if (!len) return DMB_OK;
-  if (out && out->body) {
-    if (int rc = prep_values_region(out, cfg->transfer_dtype, s)) return rc;
-  }
-  ChunkArgs a{};
-  a.geo = geometry(cfg, len);
-  if (int rc = get_basis(ctx, a.geo.s, &a.basis)) return rc;
-  a.g = grad_mean;
-  a.n_src = (int)n_members;
-  for (uint32_t q = 0; q < n_members; ++q) a.g_src[q] = members[q];
-  a.m_in = m_in;
-  a.m_out = m_out;
-  a.p_in = p_in;
-  a.p_out = p_out;
-  a.body = out ? static_cast<uint8_t*>(out->body) : nullptr;
-  a.sgd = sgd_scalars(opt->momentum_decay, lr);
-  a.status = ctx->status;
-  if (int rc = attach_fallback(ctx, &a)) return rc;
-  launch_chunk_kernel(ChunkMode::StepSgd, a, s);
-  return last_launch();
+  if (len) launch_grad_mean(members, (int)n_members, len, grad_mean, s);  // a pass of its own (SGD)
+  return dmb_step_sgd_local(ctx, grad_mean, m_in, m_out, p_in, p_out, len, opt, cfg, step, shard, lr, out, stream);
 }
 
 int dmb_step_adamw_local(dmb_ctx* ctx, const float* grad, const float* p_in, float* p_out,

@@ -540,9 +540,11 @@ __host__ __device__ constexpr uint32_t src_slot(int q) {
                    : MODE == ChunkMode::StepSgd ? OFF_ST + 2 * TILE
                                                 : (q == 1 ? OFF_SCR : (q == 2 ? OFF_ST : OFF_ST + TILE)));
 }
+// (the SGD modes' fused load measured slower in the cluster than the mean as a pass of its own,
+// and its front code cost the one-rank SGD step ~6 %: it is compiled out, the SGD *_members
+// entry points take the mean pass)
 __host__ __device__ constexpr int max_src(ChunkMode m) {
-  return m == ChunkMode::EncodeAdam ? kMaxGradSrc
-                                    : (m == ChunkMode::StepAdam || m == ChunkMode::StepSgd || m == ChunkMode::EncodeSgd) ? 2 : 0;
+  return m == ChunkMode::EncodeAdam ? kMaxGradSrc : (m == ChunkMode::StepAdam ? 2 : 0);
 }
 
 template <ChunkMode MODE, int WIRE>
