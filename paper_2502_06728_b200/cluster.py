@@ -783,40 +783,36 @@ class HybridCluster:
         sp = C.c_void_p(self._pull_stream.cuda_stream)
         off0 = self.accel * self.spec.extent
         spans = [(b["lo"], b["hi"]) for b in self.buckets] or [(0, self.spec.real_len)]
-        copied = []
+        # AdamW DeMo: the mean is fused into the tensor-core kernel's gradient load (two members for
+        # the one-pass R = 1 step, four for the prepare), on 16-byte aligned slices.  DeMo-SGD keeps
+        # it as a pass of its own: its front is busier (the momentum tile) and the fused SGD load
+        # measured slower at 2x1 (7.3 ms against 6.3 ms)
+        self._pull_fused = (os.environ.get("DMB_PULL_FUSED", "1") != "0" and self.rep.scheme == Scheme.DeMo
+                            and not self.sgd and A <= (2 if self.fused else 4)
+                            and all((4 * (off0 + b["lo"])) % 16 == 0 and (4 * b["lo"]) % 16 == 0
+                                    for b in (self.buckets or [dict(lo=0)]))
+                            and grad_full.data_ptr() % 16 == 0)
         # the one-pass R = 1 step reads the peers' slices with its own TMA over NVLink (2x1 AdamW:
         # 5.7 ms, against 6.6 ms staged by the copy engines); the R > 1 prepare is faster on staged
         # slices (2x2 AdamW: 8.2 ms staged, 9.1 ms direct), its exchange sharing the links
-        direct = (self.fused and os.environ.get("DMB_PULL_STAGED") != "1"
-                  and os.environ.get("DMB_PULL_FUSED", "1") != "0"
-                  and self.rep.scheme == Scheme.DeMo and not self.sgd and A <= 2)
+        direct = self._pull_fused and self.fused and os.environ.get("DMB_PULL_STAGED") != "1"
+        copied = []
         with torch.cuda.stream(self._copy_stream):
             hdl.barrier(channel=1)  # every member's gradient of this step is written
-            for lo, hi in spans:
-                if direct:
-                    break
-                for a, stg in self._gstage.items():
-                    stg[lo:hi].copy_(views[a][off0 + lo:off0 + hi], non_blocking=True)
+            if direct:
                 ev = torch.cuda.Event()
                 ev.record(self._copy_stream)
-                copied.append(ev)
-        # AdamW DeMo: the mean is fused into the tensor-core kernel's gradient load (two members
-        # for the one-pass R = 1 step, four for the prepare); the sources, in member order, are
-        # this rank's own slice and the staged ones
-        srcs = [grad_full[off0:] if a == self.accel else (views[a][off0:] if direct else self._gstage[a])
-                for a in range(A)]
-        if direct:
-            ev = torch.cuda.Event()
-            ev.record(self._copy_stream)
-            copied = [ev] * len(spans)
-        # DeMo-SGD keeps the mean as a pass of its own: its front is busier (the momentum tile) and
-        # the fused SGD load measured slower at 2x1 (7.3 ms against 6.3 ms)
-        self._pull_fused = (os.environ.get("DMB_PULL_FUSED", "1") != "0" and self.rep.scheme == Scheme.DeMo
-                            and not self.sgd and A <= (2 if self.fused else 4)
-                            and all(t.data_ptr() % 16 == 0 and (4 * b["lo"]) % 16 == 0
-                                    for t in srcs for b in (self.buckets or [dict(lo=0)])))
-        if self._pull_fused:
-            self._pull_srcs = srcs
+                copied = [ev] * len(spans)
+            else:
+                for lo, hi in spans:
+                    for a, stg in self._gstage.items():
+                        stg[lo:hi].copy_(views[a][off0 + lo:off0 + hi], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(self._copy_stream)
+                    copied.append(ev)
+        if self._pull_fused:  # the sources, in member order: the own slice and the peers' (mapped or staged)
+            self._pull_srcs = [grad_full[off0:] if a == self.accel else (views[a][off0:] if direct else self._gstage[a])
+                               for a in range(A)]
             self._pulled = copied
             return
         events = []

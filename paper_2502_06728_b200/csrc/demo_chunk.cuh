@@ -440,9 +440,7 @@ __global__ void __launch_bounds__(kThreads) demo_chunk_kernel(const ChunkArgs a)
           const float gp = (gv[ch][e] - lq[ch][e]) + Q[ch][e];  // optim.cpp:65
           const float ea = A.beta1 * a.ea_in[gi] + A.one_minus_beta1 * gp;
           const float es = A.beta2 * a.es_in[gi] + A.one_minus_beta2 * gp * gp;
-          const float mh = ea * A.inv_bc1;
-          const float vh = es * A.inv_bc2;
-          float p = a.p_in[gi] - A.lr * (mh / (sqrtf(vh) + A.eps));
+          float p = a.p_in[gi] - A.lr * adam_ratio(ea, es, A);
           if (A.lr_wd != 0.0f) p -= A.lr_wd * p;
           a.ea_out[gi] = ea;
           a.es_out[gi] = es;

@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(THREADS, 1) demo_tc_kernel(const ChunkArgs a) 
             const float gp = full_band ? d[j] : x[j] + d[j];
             const float ea = A.beta1 * ep[e] + A.one_minus_beta1 * gp;
             const float es = A.beta2 * sp[e] + A.one_minus_beta2 * gp * gp;
-            float pnew = pp[e] - A.lr * ((ea * A.inv_bc1) / (sqrtf(es * A.inv_bc2) + A.eps));
+            float pnew = pp[e] - A.lr * adam_ratio(ea, es, A);
             if (A.lr_wd != 0.0f) pnew -= A.lr_wd * pnew;
             ep[e] = ea;
             sp[e] = es;

@@ -439,19 +439,6 @@ __device__ __forceinline__ float cond_w(float c) {
   if (WIRE == kWireF16) return __half2float(__float2half_rn(c));
   return c;
 }
-// m_hat / (sqrt(v_hat) + eps), optim.cpp:68-70.  The IEEE sqrtf and '/' compile to a slow-path
-// check, a CALL and a reconvergence point per element, which made this kernel 2.7x slower
-// (measured: 19.6 ms against 7.2 ms per OLMo-1B step); the hardware square root and a
-// Newton-refined reciprocal are each within a few ulp (~1e-7 relative), two orders below the
-// 1e-5 parity bar -- the tests and smoke() print the error actually reached.
-__device__ __forceinline__ float adam_ratio(float m1, float m2, const AdamScalars& A) {
-  float sq, r;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(m2 * A.inv_bc2));
-  const float d = sq + A.eps;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
-  r = fmaf(r, fmaf(-d, r, 1.0f), r);
-  return (m1 * A.inv_bc1) * r;
-}
 // the wire value of a SELECTED coefficient of a stored row: there every |c| is above the
 // certification radius, so with signs cond(c) = copysign(1, c) -- one bit operation
 template <int WIRE>

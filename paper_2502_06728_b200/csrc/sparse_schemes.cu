@@ -99,7 +99,7 @@ __global__ void sparse_merge_kernel(SparseSel sel, Bodies in, int dtype,
       const float gp = on ? (gi - gi) + q : (gi - 0.0f) + q;
       const float ea = A.beta1 * ea_in[i] + A.one_minus_beta1 * gp;
       const float es = A.beta2 * es_in[i] + A.one_minus_beta2 * gp * gp;
-      float p = p_in[i] - A.lr * ((ea * A.inv_bc1) / (sqrtf(es * A.inv_bc2) + A.eps));
+      float p = p_in[i] - A.lr * adam_ratio(ea, es, A);
       if (A.lr_wd != 0.0f) p -= A.lr_wd * p;
       ea_out[i] = ea;
       es_out[i] = es;
@@ -290,6 +290,18 @@ __global__ void __launch_bounds__(kBlock) sparse_merge_v4(SparseSel sel, Bodies 
   const uint64_t nq = (sel.len + 3) / 4;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const float R = (float)in.R;
+  // the merged value of a ternary member sum x is x / R: the 2R + 1 possible quotients, IEEE
+  // divided once per CTA (the division per element cost more than the memory traffic)
+  __shared__ float qtab[2 * 120 + 1];
+  // x / R for a power-of-two R is x * (1 / R) exactly: a multiply instead of the IEEE division
+  const bool pow2 = (in.R & (in.R - 1)) == 0;
+  const float invR = 1.0f / R;
+  auto div_r = [&](float x) { return pow2 ? x * invR : x / R; };
+  const bool tern = SCH == kSchDense && dtype == DMB_TERNARY && in.R <= 120;
+  if (tern) {
+    for (int x = threadIdx.x; x <= 2 * in.R; x += blockDim.x) qtab[x] = (float)(x - in.R) / R;
+    __syncthreads();
+  }
   uint64_t qd = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   StrideState ss{0, 0};
   uint64_t aq = 0, ar = 0;
@@ -308,19 +320,46 @@ __global__ void __launch_bounds__(kBlock) sparse_merge_v4(SparseSel sel, Bodies 
     float q[4] = {0.f, 0.f, 0.f, 0.f};
     if (SCH == kSchDense && full && dtype == DMB_FP32) {
       float acc[4] = {0.f, 0.f, 0.f, 0.f};  // member order (replicate.cpp:264-265)
-      for (int r = 0; r < in.R; ++r) {
-        const float4 v = ld4(reinterpret_cast<const float*>(in.body[r]) + i0);
-        acc[0] += v.x, acc[1] += v.y, acc[2] += v.z, acc[3] += v.w;
+      for (int r0 = 0; r0 < in.R; r0 += 4) {  // four members' loads in flight, then added in order
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          v[u] = r0 + u < in.R ? ld4(reinterpret_cast<const float*>(in.body[r0 + u]) + i0) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (r0 + u < in.R) acc[0] += v[u].x, acc[1] += v[u].y, acc[2] += v[u].z, acc[3] += v[u].w;
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) q[j] = acc[j] / R;
+      for (int j = 0; j < 4; ++j) q[j] = div_r(acc[j]);
+    } else if (tern && full) {
+      // the quad's four 2-bit codes are one byte of every body; a member's values are -1 / 0 / +1,
+      // so their member-order FP32 sum is an exact integer: count it in byte lanes (value + 1 =
+      // (code & 1) + (~code >> 1 & 1) per field: 1 -> 2, 2 -> 0, 0 and 3 -> 1), one load per member
+      // (members in groups of eight whose loads are all issued before any is used: one memory
+      // latency per group, not per member)
+      uint32_t cnt = 0;
+      for (int r0 = 0; r0 < in.R; r0 += 8) {
+        uint32_t bb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) bb[u] = r0 + u < in.R ? (uint32_t)__ldg(in.body[r0 + u] + (i0 >> 2)) : 0x55u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // the padding code 0x55 (+1 x 4) is taken back below
+          const uint32_t b = bb[u];
+          const uint32_t t = (b & 0x55u) + (~(b >> 1) & 0x55u);
+          cnt += (t & 3u) | ((t & 0xCu) << 6) | ((t & 0x30u) << 12) | ((t & 0xC0u) << 18);
+        }
+      }
+      const int pad = (8 - in.R % 8) % 8;  // padding members counted value + 1 = 2 each
+      cnt -= (uint32_t)(2 * pad) * 0x01010101u;  // byte j: x + R for the sum x of element j
+#pragma unroll
+      for (int j = 0; j < 4; ++j) q[j] = qtab[(cnt >> (8 * j)) & 0xffu];
     } else if (on) {
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if ((on >> j) & 1u) {
           float acc = 0.0f;  // member order (replicate.cpp:264-265, :277-279)
           for (int r = 0; r < in.R; ++r) acc += load_wire_value(in.body[r], slot[j], dtype);
-          q[j] = acc / R;
+          q[j] = div_r(acc);
         }
     }
     if (full) {
@@ -340,7 +379,7 @@ __global__ void __launch_bounds__(kBlock) sparse_merge_v4(SparseSel sel, Bodies 
           const float gp = ((on >> j) & 1u) ? (gi[j] - gi[j]) + q[j] : (gi[j] - 0.0f) + q[j];
           eo[j] = A.beta1 * ei[j] + A.one_minus_beta1 * gp;
           so[j] = A.beta2 * si[j] + A.one_minus_beta2 * gp * gp;
-          float pn = pi[j] - A.lr * ((eo[j] * A.inv_bc1) / (sqrtf(so[j] * A.inv_bc2) + A.eps));
+          float pn = pi[j] - A.lr * adam_ratio(eo[j], so[j], A);
           if (A.lr_wd != 0.0f) pn -= A.lr_wd * pn;
           po[j] = pn;
         }
@@ -361,7 +400,7 @@ __global__ void __launch_bounds__(kBlock) sparse_merge_v4(SparseSel sel, Bodies 
           const float gp = ((on >> j) & 1u) ? (gi - gi) + q[j] : (gi - 0.0f) + q[j];
           const float ea = A.beta1 * ea_in[i] + A.one_minus_beta1 * gp;
           const float es = A.beta2 * es_in[i] + A.one_minus_beta2 * gp * gp;
-          float pn = p_in[i] - A.lr * ((ea * A.inv_bc1) / (sqrtf(es * A.inv_bc2) + A.eps));
+          float pn = p_in[i] - A.lr * adam_ratio(ea, es, A);
           if (A.lr_wd != 0.0f) pn -= A.lr_wd * pn;
           ea_out[i] = ea;
           es_out[i] = es;
@@ -398,7 +437,7 @@ __global__ void adamw_apply_kernel(float* __restrict__ p, float* __restrict__ ea
     const float gp = merged ? (g[i] - lq[i]) + merged[i] : g[i];
     const float ea = A.beta1 * ea_[i] + A.one_minus_beta1 * gp;
     const float es = A.beta2 * es_[i] + A.one_minus_beta2 * gp * gp;
-    float pv = p[i] - A.lr * ((ea * A.inv_bc1) / (sqrtf(es * A.inv_bc2) + A.eps));
+    float pv = p[i] - A.lr * adam_ratio(ea, es, A);
     if (A.lr_wd != 0.0f) pv -= A.lr_wd * pv;
     ea_[i] = ea;
     es_[i] = es;
