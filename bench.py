@@ -49,8 +49,9 @@ def parse():
     ap.add_argument("--sign", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--buckets", type=int, default=4,
-                    help="N>1: chunk-aligned buckets of the shard pipelined through prepare / all-gather / merge")
+    ap.add_argument("--buckets", type=int, default=None,
+                    help="N>1: chunk-aligned buckets of the shard pipelined through prepare / all-gather / merge "
+                         "(default: 4 at S = 1, 8 at S > 1, where they also pipeline the reduce-scatter)")
     ap.add_argument("--wire", choices=["mask", "reference"], default="mask",
                     help="N>1 DeMo exchange layout: lossless u64-mask + packed values, or the reference body")
     ap.add_argument("--sm-reserve", type=int, default=0,
@@ -281,6 +282,8 @@ def run_ours(args, rank, world, local_rank):
         topo = Topology(nodes=R, accels_per_node=S)
         sg, rg = groups_for(topo, rank)
         os.environ["DMB_SM_RESERVE"] = str(args.sm_reserve)
+        if args.buckets is None:
+            args.buckets = 4 if S == 1 else 8
         cluster = HybridCluster(topo, L, opt, cfg, params, rank, sg, rg, buckets=args.buckets, wire=args.wire,
                                 pull_grads=bool(args.pull_rs) and S > 1, pull_ctas=args.pull_ctas)
         del params
