@@ -1665,7 +1665,7 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
   float* bt = reinterpret_cast<float*>(fsm + S * S * 4);    // B^T: (i, j) at i*64 + j
   double* xw = reinterpret_cast<double*>(fsm + S * S * 8) + (threadIdx.x >> 5) * S;  // this warp's chunk
   float* xf = reinterpret_cast<float*>(xw);
-  if (*a.fb_count == 0) return;
+  if (*a.fb_count <= blockIdx.x * kFixWarps) return;  // no listed chunk for this CTA: skip the basis load
   if (!kEncodeOnly && step_failed(a.status)) return;
   for (int u = 4 * threadIdx.x; u < S * S; u += 4 * blockDim.x) {
     *reinterpret_cast<float4*>(b32 + u) = __ldg(reinterpret_cast<const float4*>(a.basis.B + u));
