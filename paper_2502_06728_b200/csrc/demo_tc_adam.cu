@@ -1442,14 +1442,14 @@ __global__ void __maxnreg__(128)
                 gq[2 * r + 1] = b1 ? gq[2 * r + 1] + v1 : gq[2 * r + 1];
               }
             };
-            if (vd == DMB_FP32) {
-              const float* f = reinterpret_cast<const float*>(sv);
-              auto ld = [&](uint32_t t) { return f[t]; };
+            if constexpr (WIRE == kWireF16) {  // the value type is the kernel's (one loop compiled)
+              const __half* h = reinterpret_cast<const __half*>(sv);
+              auto ld = [&](uint32_t t) { return __half2float(h[t]); };
               add_row(gq0, tb0, rk0, o0, ld);
               add_row(gq1, tb1, rk1, o1, ld);
             } else {
-              const __half* h = reinterpret_cast<const __half*>(sv);
-              auto ld = [&](uint32_t t) { return __half2float(h[t]); };
+              const float* f = reinterpret_cast<const float*>(sv);
+              auto ld = [&](uint32_t t) { return f[t]; };
               add_row(gq0, tb0, rk0, o0, ld);
               add_row(gq1, tb1, rk1, o1, ld);
             }
