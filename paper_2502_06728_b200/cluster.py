@@ -29,6 +29,20 @@ One step runs in three phases (`begin`, `agree`, `commit`; `step` runs all three
 At R = 1 (S x 1 layouts) there is nothing to exchange and DeMo runs the fused one-pass step
 kernel with double-buffered outputs, swapped when the step succeeds.
 
+The shard group's reduce-scatter is NCCL's, or -- HybridCluster(pull_grads=True), gradients
+written into grad_buffer(step) (symmetric memory) -- fused into the step kernels: the AdamW
+prepare / one-pass step average the members' slices of the shard in their gradient load
+(dmb_*_members; the peers' slices read over NVLink by the kernel's TMA for the one-pass step,
+staged by the copy engines for the prepare), DeMo-SGD takes the mean as a CTA-budgeted pass of
+its own (dmb_grad_mean_pull) beside the step kernels; every variant is bit-identical to NCCL's.
+
+Environment switches (measurement and fallbacks; the defaults are the measured best):
+  DMB_CE_GATHER=0      replica exchange by NCCL all-gather instead of copy engines
+  DMB_GATHER_BUDGET=n  exchange memory budget in bytes (above it: memory-bounded windows)
+  DMB_OVERLAP=1        overlapped merges on split SMs (DMB_MERGE_SMS: the merges' share)
+  DMB_PULL_FUSED=0     pulled reduce-scatter as a mean pass even for AdamW
+  DMB_PULL_STAGED=1    stage the peers' slices by copy engines for the one-pass step too
+
 The exchange is injectable: `CollectiveExchange` (torch.distributed all-gather, any
 backend), `CopyEngineExchange` (symmetric memory pulled by copy engines over NVLink, NCCL
 only for the agreement), `LocalExchange` (R members in one process on one GPU, tests).  The
