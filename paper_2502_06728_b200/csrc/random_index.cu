@@ -13,7 +13,7 @@
 // probability < 2^-32, and a rejection shifts every later draw by one output, so the CTAs
 // assume none and report the first output that could be one -- an exact sequential
 // replay from that substream fixes the rare case; (2) for every position t, first[t]/second[t]
-// hold the two smallest iterations that targeted it (atomicMin passes); (3) the
+// hold the two smallest iterations that targeted it (one atomicMin pass); (3) the
 // value that ends in position x < count is resolved by following
 //   D(i) = value at position i-1 just before iteration i
 //        = D(min{i' > i : j_i' = i-1})  or  i-1 if there is none
@@ -445,20 +445,18 @@ const DevPositions* jump_polys(uint64_t W, uint64_t blocks, int device, const ch
   return &d;
 }
 
-__global__ void first_pass(const uint32_t* __restrict__ draws, uint64_t len, uint64_t ndraws,
-                           uint32_t* __restrict__ first) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t d = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; d < ndraws; d += stride)
-    atomicMin(&first[draws[d]], (uint32_t)(len - d));
-}
-
-__global__ void second_pass(const uint32_t* __restrict__ draws, uint64_t len, uint64_t ndraws,
-                            const uint32_t* __restrict__ first, uint32_t* __restrict__ second) {
+// first[t] / second[t]: the two smallest iterations that targeted position t, in one pass.  The
+// atomicMin on first returns what it displaced: every iteration but the smallest is displaced or
+// loses at some point, and the loser of each exchange (the larger of the two) goes to second, so
+// second ends as the smallest of all but the first (iterations are distinct)
+__global__ void touch_pass(const uint32_t* __restrict__ draws, uint64_t len, uint64_t ndraws,
+                           uint32_t* __restrict__ first, uint32_t* __restrict__ second) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t d = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; d < ndraws; d += stride) {
     const uint32_t tgt = draws[d];
     const uint32_t it = (uint32_t)(len - d);
-    if (first[tgt] != it) atomicMin(&second[tgt], it);
+    const uint32_t old = atomicMin(&first[tgt], it);
+    if (old != kNone) atomicMin(&second[tgt], old > it ? old : it);
   }
 }
 
@@ -649,7 +647,7 @@ int launch_random_indices(uint64_t engine_seed, uint64_t len, uint64_t count, co
     }
     const DevPositions* jp = jump_polys(W, nsub, dev, err);
     if (!jp) return DMB_CUDA;
-    count_launches(9);
+    count_launches(8);
     // DMB_MT_FORCE_FIXUP=1 (tests): report a rejection at output 0, so the sequential replay
     // rewrites every draw -- it must reproduce the substreams' draws exactly
     const char* ff = std::getenv("DMB_MT_FORCE_FIXUP");
@@ -667,8 +665,7 @@ int launch_random_indices(uint64_t engine_seed, uint64_t len, uint64_t count, co
     mt_fixup_kernel<<<1, kMtThreads, 0, stream>>>(s.mt_windows, W, len, ndraws, s.draws, s.mt_reject);
     cudaMemsetAsync(s.first, 0xff, len * sizeof(uint32_t), stream);
     cudaMemsetAsync(s.second, 0xff, len * sizeof(uint32_t), stream);
-    first_pass<<<sm_grid(ndraws, 256), 256, 0, stream>>>(s.draws, len, ndraws, s.first);
-    second_pass<<<sm_grid(ndraws, 256), 256, 0, stream>>>(s.draws, len, ndraws, s.first, s.second);
+    touch_pass<<<sm_grid(ndraws, 256), 256, 0, stream>>>(s.draws, len, ndraws, s.first, s.second);
     resolve_kernel<<<sm_grid(count, 256), 256, 0, stream>>>(count, s.first, s.second, s.bitmap);
   }
   const uint64_t blocks = (words + kScanBlock - 1) / kScanBlock;
