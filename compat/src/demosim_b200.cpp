@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -544,48 +545,145 @@ void baseline_adamw_step(std::span<double> params, MomentumState& state, std::sp
   adamw_apply(params, state, grad, grad, nullptr, opt, lr);
 }
 
-// ---- model.hpp: the quadratic bowl (model.cpp:99-111, :144-155) ------------------------------
-std::size_t Model::param_count() const {
-  if (kind != ModelKind::Quadratic) throw ConfigError("the MLP toy model is outside the facade");
-  return layer_dims.front();
+// ---- model.hpp (model.cpp:121-244): the toy producers on the device -----------------------------
+// loss and gradient of a host batch by dmb_toy_loss_grad / dmb_toy_loss: the batch becomes the
+// pool (identity order, one worker), parameters go to the device as FP32 and the FP64 loss and
+// the FP32 gradient come back; init_params draws on the host (the reference's Rng)
+std::size_t Model::param_count() const {  // model.cpp:121-125
+  if (kind == ModelKind::Quadratic) return layer_dims.front();
+  std::size_t total = 0;
+  for (std::size_t l = 0; l + 1 < layer_dims.size(); ++l) total += layer_dims[l + 1] * layer_dims[l] + layer_dims[l + 1];
+  return total;
 }
 
-static void check_quadratic(const Model& model, std::span<const double> params, const Batch& batch) {
-  if (model.kind != ModelKind::Quadratic) throw ConfigError("the MLP toy model is outside the facade");
-  if (params.size() < model.layer_dims.front() || batch.inputs.size() < batch.size * model.layer_dims.front())
-    throw ConfigError("batch or parameters too short for the model");
+static void check_batch(const Model& model, std::span<const double> params, const Batch& batch) {  // model.cpp:13-35
+  char buf[160];
+  if (params.size() < model.param_count()) {
+    std::snprintf(buf, sizeof buf, "parameter vector too short: %zu < %zu", params.size(), model.param_count());
+    throw ConfigError(buf);
+  }
+  if (batch.size == 0) throw ConfigError("empty batch");
+  if (batch.input_dim != model.input_dim()) {
+    std::snprintf(buf, sizeof buf, "batch input dim %zu does not match model input dim %zu", batch.input_dim,
+                  model.input_dim());
+    throw ConfigError(buf);
+  }
+  if (model.kind == ModelKind::Mlp) {
+    if (model.loss == LossKind::CrossEntropy) {
+      if (batch.labels.size() != batch.size) throw ConfigError("cross entropy batch is missing labels");
+    } else if (batch.targets.size() != batch.size * model.output_dim()) {
+      throw ConfigError("regression batch targets do not match model output dim");
+    }
+  }
+  if (model.layer_dims.size() > 9) throw ConfigError("the device producer takes at most 8 layers");
 }
+
+namespace {
+struct DevBatch {  // a host batch as a device pool
+  std::unique_ptr<Dev> in, tgt, lab;
+  dmb_toy_pool pool{};
+  DevBatch(const Model& m, const Batch& b) {
+    auto put = [](const void* src, size_t bytes) {
+      auto d = std::make_unique<Dev>(bytes);
+      if (bytes && cudaMemcpy(d->p, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+        throw std::runtime_error("CUDA: upload failed");
+      return d;
+    };
+    in = put(b.inputs.data(), b.size * b.input_dim * 8);
+    pool.inputs = static_cast<const double*>(in->p);
+    if (m.kind == ModelKind::Mlp && m.loss == LossKind::Mse) {
+      tgt = put(b.targets.data(), b.targets.size() * 8);
+      pool.targets = static_cast<const double*>(tgt->p);
+    }
+    if (m.kind == ModelKind::Mlp && m.loss == LossKind::CrossEntropy) {
+      std::vector<int32_t> l(b.labels.begin(), b.labels.end());
+      lab = put(l.data(), l.size() * 4);
+      pool.labels = static_cast<const int32_t*>(lab->p);
+    }
+    pool.size = b.size;
+  }
+};
+dmb_toy_model toy_of(const Model& m) {
+  dmb_toy_model t{};
+  t.kind = m.kind == ModelKind::Quadratic ? 0u : 1u;
+  t.activation = m.activation == Activation::Tanh ? 0u : 1u;
+  t.loss = m.loss == LossKind::Mse ? 0u : 1u;
+  t.n_dims = (uint32_t)m.layer_dims.size();
+  for (size_t l = 0; l < m.layer_dims.size(); ++l) t.dims[l] = (uint32_t)m.layer_dims[l];
+  return t;
+}
+double loss_of(const Dev& loss) {
+  double h = 0.0;
+  if (cudaMemcpy(&h, loss.p, 8, cudaMemcpyDeviceToHost) != cudaSuccess) throw std::runtime_error("CUDA: download failed");
+  return h;
+}
+}  // namespace
 
 double forward_loss(const Model& model, std::span<const double> params, const Batch& batch) {
-  check_quadratic(model, params, batch);
-  const size_t dim = model.layer_dims.front();
-  double acc = 0.0;  // mean over the batch of 1/2 |theta - x_i|^2
-  for (size_t i = 0; i < batch.size; ++i) {
-    double sq = 0.0;
-    for (size_t k = 0; k < dim; ++k) {
-      const double diff = params[k] - batch.inputs[i * dim + k];
-      sq += diff * diff;
-    }
-    acc += 0.5 * sq;
-  }
-  return acc / static_cast<double>(batch.size);
+  check_batch(model, params, batch);
+  const dmb_toy_model t = toy_of(model);
+  DevBatch db(model, batch);
+  auto p = to_device(params.first(model.param_count()));
+  Dev loss(8);
+  check(dmb_toy_loss(ctx(), &t, &db.pool, p->f(), static_cast<double*>(loss.p), nullptr));
+  status();
+  return loss_of(loss);
 }
 
 LossAndGradient loss_and_gradient(const Model& model, std::span<const double> params, const Batch& batch) {
+  check_batch(model, params, batch);
+  const dmb_toy_model t = toy_of(model);
+  DevBatch db(model, batch);
+  auto p = to_device(params);
+  std::vector<int64_t> order(batch.size);
+  for (size_t i = 0; i < batch.size; ++i) order[i] = (int64_t)i;
+  Dev dord(order.size() * 8), g(params.size() * 4), loss(8);
+  if (cudaMemcpy(dord.p, order.data(), order.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess)
+    throw std::runtime_error("CUDA: upload failed");
+  check(dmb_toy_loss_grad(ctx(), &t, &db.pool, static_cast<const int64_t*>(dord.p), 0, batch.size, p->f(),
+                          params.size(), 1, 1, g.f(), params.size(), static_cast<double*>(loss.p), nullptr));
+  status();
   LossAndGradient r;
-  r.loss = forward_loss(model, params, batch);
-  r.grad.assign(params.size(), 0.0);  // the pad tail gets exact zeros
-  const size_t dim = model.layer_dims.front();
-  for (size_t k = 0; k < dim; ++k) {  // theta - mean(x)
-    double s = 0.0;
-    for (size_t i = 0; i < batch.size; ++i) s += batch.inputs[i * dim + k];
-    r.grad[k] = params[k] - s / static_cast<double>(batch.size);
-  }
+  r.loss = loss_of(loss);
+  r.grad = from_device(g.f(), params.size());  // the pad tail gets exact zeros
   return r;
 }
 
 DenseVector gradient(const Model& model, std::span<const double> params, const Batch& batch) {
   return loss_and_gradient(model, params, batch).grad;
+}
+
+DenseVector finite_diff_gradient(const Model& model, std::span<const double> params, const Batch& batch,
+                                 double h) {  // model.cpp:209-222
+  if (!(h > 0.0)) throw ConfigError("finite difference step must be positive");
+  DenseVector theta(params.begin(), params.end());
+  DenseVector out(params.size(), 0.0);
+  for (size_t i = 0; i < theta.size(); ++i) {
+    const double saved = theta[i];
+    theta[i] = saved + h;
+    const double up = forward_loss(model, theta, batch);
+    theta[i] = saved - h;
+    const double down = forward_loss(model, theta, batch);
+    theta[i] = saved;
+    out[i] = (up - down) / (2.0 * h);
+  }
+  return out;
+}
+
+DenseVector init_params(const Model& model, uint64_t seed, std::size_t padded_len) {  // model.cpp:224-244
+  const size_t n = model.param_count();
+  if (padded_len < n) throw ConfigError("padded parameter length shorter than the model");
+  DenseVector params(padded_len, 0.0);
+  if (model.kind == ModelKind::Quadratic) return params;
+  Rng rng(mix_seed(seed, 0x6d6f64656cULL));
+  size_t off = 0;
+  for (size_t l = 0; l + 1 < model.layer_dims.size(); ++l) {
+    const size_t in = model.layer_dims[l], out = model.layer_dims[l + 1];
+    const double bound = 1.0 / std::sqrt(static_cast<double>(in));
+    for (size_t k = 0; k < out * in + out; ++k) params[off + k] = rng.uniform(-bound, bound);
+    off += out * in + out;
+  }
+  return params;
 }
 
 }  // namespace demosim
