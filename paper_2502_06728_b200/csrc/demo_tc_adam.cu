@@ -1638,25 +1638,51 @@ teardown:
 
 // ---------------------------------------------------------------------------
 // Fix-up of the full chunks the tensor-core kernel could not certify (fb_list): one warp
-// per chunk, lane j holds coefficients j and j+32.  First an FP32 pass: the coefficients
-// by eight FMA chains and a summation tree, whose error against the oracle's FP64 values is
-// rigorously below kFmaEps * ||x||_1 (gamma_11 + u for the rounded basis, times max|B| =
-// sqrt(2/64)) -- 13x tighter than the tensor-core kernel's 3xTF32 radius, so nearly every
-// deferred chunk settles here.  A chunk it cannot certify either is re-derived in FP64 in the oracle's operation
-// order (acc = 0; acc = acc + B[j][i]*x_i, ascending i, no FMA: transform.cpp:56-63) from
-// the FP64 basis, and the TopK is exact on those values (ties toward the
-// lower index, transform.cpp:127-133).  Then the chunk gets the same wire values, payload
-// and W = wire - coef -> D = IDCT(W) -> AdamW as in the main kernel (whose apply warps left
-// this chunk's state untouched).
+// per chunk, lane j holds coefficients j and j+32.  First an FP32 pass on the folded chunk
+// (B[j][63-i] = (-1)^j B[j][i], so c_j = sum_{i<32} B[j][i] (x_i +- x_{63-i}), + for even j):
+// 32 terms per coefficient by eight FMA chains and a summation tree, whose error against the
+// oracle's FP64 values is rigorously below kFmaEps * ||x||_1 (the fold's rounding u, gamma_7 of
+// the chains and the tree, u for the rounded basis: 9u times max|B| = sqrt(2/64); 14u is
+// used) -- far tighter than the tensor-core kernel's 3xTF32 radius, so nearly every deferred
+// chunk settles here; its TopK threshold comes from a warp bitonic sort of the 64 keys.  A chunk
+// it cannot certify either is re-derived in FP64 in the oracle's operation order (acc = 0;
+// acc = acc + B[j][i]*x_i, ascending i, no FMA: transform.cpp:56-63) from the FP64 basis, and
+// the TopK is exact on those values (ties toward the lower index, transform.cpp:127-133).
+// Then the chunk gets the same wire values, payload and W = wire - coef -> D = IDCT(W) ->
+// AdamW as in the main kernel (whose apply warps left this chunk's state untouched); the
+// inverse uses the same symmetry: lane l computes D_l and D_{63-l} from the even and odd j.
 constexpr int kFixWarps = 8;
 // B row-major, B^T, then x per warp (FP64, or FP32 in the FMA pass); the rare FP64 pass
 // reads the FP64 basis through L1
 constexpr uint32_t FIX_SMEM = S * S * 4 + S * S * 4 + kFixWarps * S * 8;
-// gamma_11 of the chains and the tree plus u for the FP32 basis: 12 * 2^-24, with margin
+// 9u bound above, with margin
 constexpr float kFmaEps = 14.0f * 5.9604645e-8f * 0.17677669f;
 
+// the 64 keys of a warp (column lane in v0, lane + 32 in v1) sorted descending: afterwards
+// lane l holds sorted[l] in v0 and sorted[l + 32] in v1
+__device__ __forceinline__ void bitonic64_desc(uint32_t& v0, uint32_t& v1) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 64; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride == 32) {  // in-lane, size 64: one descending block, column lane the lower index
+        const uint32_t hi = max(v0, v1);
+        v1 = min(v0, v1);
+        v0 = hi;
+      } else {
+        const bool lower = (lane & stride) == 0;
+        const uint32_t p0 = __shfl_xor_sync(kFull, v0, stride), p1 = __shfl_xor_sync(kFull, v1, stride);
+        const bool d0 = (lane & size) == 0, d1 = ((lane + 32) & size) == 0;  // descending blocks
+        v0 = lower == d0 ? max(v0, p0) : min(v0, p0);
+        v1 = lower == d1 ? max(v1, p1) : min(v1, p1);
+      }
+    }
+  }
+}
+
 template <ChunkMode MODE, int WIRE>
-__global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkArgs a) {
+__global__ void __launch_bounds__(kFixWarps * 32, 6) demo_fix64_kernel(const ChunkArgs a) {
   constexpr bool kEncodeOnly = MODE == ChunkMode::EncodeAdam;
   constexpr bool kSgd = MODE == ChunkMode::StepSgd;
   constexpr bool kMomentum = kSgd || MODE == ChunkMode::EncodeSgd;
@@ -1682,10 +1708,27 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
   const unsigned n = *a.fb_count;
   if (blockIdx.x == 0 && threadIdx.x == 0 && a.status) atomicAdd(&a.status->fallback_chunks, (unsigned long long)n);
   const unsigned nwarps = gridDim.x * kFixWarps;
-  for (unsigned u = blockIdx.x * kFixWarps + (threadIdx.x >> 5); u < n; u += nwarps) {
-    const uint64_t c = a.fb_list[u];
+  // every load of a chunk is issued up front (one memory round trip per chunk, the next list
+  // entry prefetched); the state entries a lane updates are columns lane and 63 - lane
+  constexpr bool kAdamState = !kEncodeOnly && !kMomentum;
+  unsigned u = blockIdx.x * kFixWarps + (threadIdx.x >> 5);
+  uint64_t c_next = u < n ? a.fb_list[u] : 0;
+  for (; u < n; u += nwarps) {
+    const uint64_t c = c_next;
+    if (u + nwarps < n) c_next = a.fb_list[u + nwarps];
     const uint64_t g0 = c * S;
     float x0 = a.g[g0 + lane], x1 = a.g[g0 + lane + 32];
+    float st_p[2] = {0.0f, 0.0f}, st_m1[2] = {0.0f, 0.0f}, st_m2[2] = {0.0f, 0.0f};
+    if (kAdamState || kSgd) {
+      st_p[0] = a.p_in[g0 + lane];
+      st_p[1] = a.p_in[g0 + 63 - lane];
+    }
+    if (kAdamState) {
+      st_m1[0] = a.ea_in[g0 + lane];
+      st_m1[1] = a.ea_in[g0 + 63 - lane];
+      st_m2[0] = a.es_in[g0 + lane];
+      st_m2[1] = a.es_in[g0 + 63 - lane];
+    }
     if (kMomentum) {  // the encoded vector is m_acc = beta m + g (multiply, then add)
       x0 = __fadd_rn(__fmul_rn(a.sgd.beta, a.m_in[g0 + lane]), x0);
       x1 = __fadd_rn(__fmul_rn(a.sgd.beta, a.m_in[g0 + lane + 32]), x1);
@@ -1694,19 +1737,19 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
     float c0f = 0.0f, c1f = 0.0f, w0 = 0.0f, w1 = 0.0f;
     __syncwarp();  // the previous chunk's reads of this warp's x buffer are done
     if (!a.force_fp64) {
-      // ---- FP32 pass: FMA chains (two partial sums per coefficient) + certification ----
-      xf[lane] = x0;
-      xf[lane + 32] = x1;
+      // ---- FP32 pass on the folded chunk + certification ----
+      const float xr = __shfl_sync(kFull, x1, 31 - lane);  // x_{63-lane}
+      xf[lane] = x0 + xr;       // y+
+      xf[36 + lane] = x0 - xr;  // y- (offset: the halves a warp reads at once sit in different banks)
       __syncwarp();
-      // eight FMA chains of eight terms per coefficient, then a depth-3 tree: the rounding
-      // error is within gamma_11 of sum |b x| (gamma_64 for one chain)
+      // eight FMA chains of four terms per coefficient, then a depth-3 tree
       float s0[8], s1[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) s0[e] = s1[e] = 0.0f;
-      const float4* x4 = reinterpret_cast<const float4*>(xf);
+      const float4* y4 = reinterpret_cast<const float4*>(xf + ((lane & 1) ? 36 : 0));
 #pragma unroll
-      for (int q = 0; q < S / 4; ++q) {
-        const float4 v = x4[q];  // broadcast read
+      for (int q = 0; q < S / 8; ++q) {
+        const float4 v = y4[q];
         const float* r = bt + 4 * q * S;
         const int e = (4 * q) & 7;
         s0[e] = fmaf(r[lane], v.x, s0[e]);
@@ -1726,30 +1769,15 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
       const float eps = kFmaEps * l1;
       const uint32_t q0 = __float_as_uint(fabsf(f0)), q1 = __float_as_uint(fabsf(f1));
       bool ok = true, fs0 = true, fs1 = true;
-      if (!full_band) {  // the k-th largest key by MSB radix select; ties are left to FP64
-        const uint32_t mx = __reduce_max_sync(kFull, max(q0, q1)), mn = __reduce_min_sync(kFull, min(q0, q1));
-        const uint32_t diff = mx ^ mn;
-        const int top = diff ? 31 - __clz((int)diff) : -1;
-        uint32_t T = top >= 0 ? (mx & ~((2u << top) - 1u)) : mx;
-        ok = false;
-        for (int b = top; b >= 0; --b) {
-          const uint32_t cand = T | (1u << b);
-          const int cnt = __popc(__ballot_sync(kFull, q0 >= cand)) + __popc(__ballot_sync(kFull, q1 >= cand));
-          if (cnt >= k) {
-            T = cand;
-            if (cnt == k) {
-              ok = true;
-              break;
-            }
-          }
-        }
-        fs0 = q0 >= T;
-        fs1 = q1 >= T;
-        if (ok) {
-          const float kth = __uint_as_float(__reduce_min_sync(kFull, min(fs0 ? q0 : ~0u, fs1 ? q1 : ~0u)));
-          const float nxt = __uint_as_float(__reduce_max_sync(kFull, max(fs0 ? 0u : q0, fs1 ? 0u : q1)));
-          ok = kth - nxt > 2.0f * eps && (!need_signs || kth > eps);
-        }
+      if (!full_band) {  // the k-th and (k+1)-th largest keys; a tie fails the gap and goes to FP64
+        uint32_t v0 = q0, v1 = q1;
+        bitonic64_desc(v0, v1);
+        const uint32_t kb = __shfl_sync(kFull, k - 1 < 32 ? v0 : v1, (k - 1) & 31);
+        const uint32_t nb = __shfl_sync(kFull, k < 32 ? v0 : v1, k & 31);
+        const float kth = __uint_as_float(kb), nxt = __uint_as_float(nb);
+        ok = kth - nxt > 2.0f * eps && (!need_signs || kth > eps);  // implies exactly k keys >= kth
+        fs0 = q0 >= kb;
+        fs1 = q1 >= kb;
       } else if (need_signs) {
         ok = __uint_as_float(__reduce_min_sync(kFull, min(q0, q1))) > eps;
       }
@@ -1856,55 +1884,76 @@ __global__ void __launch_bounds__(kFixWarps * 32) demo_fix64_kernel(const ChunkA
       }
     }
     if (kEncodeOnly) continue;
-    if (kMomentum) {  // local_q = IDCT(coef), Q = IDCT(wire) over the selection, ascending j
-      float q0 = 0.0f, q1 = 0.0f, l0 = 0.0f, l1 = 0.0f;
-      for (int e = 0; e < 2; ++e) {
-        unsigned m = __ballot_sync(kFull, e ? sel1 : sel0);
-        while (m) {
-          const int l = __ffs(m) - 1;
-          m &= m - 1;
-          const int j = l + 32 * e;
-          const float wj = __shfl_sync(kFull, e ? w1 : w0, l);
-          const float cj = __shfl_sync(kFull, e ? c1f : c0f, l);
-          q0 = fmaf(wj, b32[j * S + lane], q0);
-          q1 = fmaf(wj, b32[j * S + lane + 32], q1);
-          l0 = fmaf(cj, b32[j * S + lane], l0);
-          l1 = fmaf(cj, b32[j * S + lane + 32], l1);
+    // the inverses by the basis symmetry: lane l computes entries l and 63 - l from the even
+    // and odd j sums (entry 63 - l pairs with x_{63-l}, x1 of lane 31 - l)
+    const float xr = __shfl_sync(kFull, x1, 31 - lane);
+    float* wv = reinterpret_cast<float*>(xw);
+    __syncwarp();  // the passes' reads of this warp's buffer are done
+    if (kMomentum) {  // local_q = IDCT(coef), Q = IDCT(wire) over the selection
+      wv[lane] = sel0 ? c0f : 0.0f;
+      wv[lane + 32] = sel1 ? c1f : 0.0f;
+      if (kSgd) {
+        wv[64 + lane] = sel0 ? w0 : 0.0f;
+        wv[96 + lane] = sel1 ? w1 : 0.0f;
+      }
+      __syncwarp();
+      float le = 0.0f, lo = 0.0f, qe = 0.0f, qo = 0.0f;
+      const float4* l4 = reinterpret_cast<const float4*>(wv);
+      const float4* q4 = reinterpret_cast<const float4*>(wv + 64);
+#pragma unroll 4
+      for (int q = 0; q < S / 4; ++q) {
+        const float* b = b32 + 4 * q * S + lane;
+        const float4 c = l4[q];
+        le = fmaf(c.x, b[0], le);
+        lo = fmaf(c.y, b[S], lo);
+        le = fmaf(c.z, b[2 * S], le);
+        lo = fmaf(c.w, b[3 * S], lo);
+        if (kSgd) {
+          const float4 w = q4[q];
+          qe = fmaf(w.x, b[0], qe);
+          qo = fmaf(w.y, b[S], qo);
+          qe = fmaf(w.z, b[2 * S], qe);
+          qo = fmaf(w.w, b[3 * S], qo);
         }
       }
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const uint64_t gi = g0 + lane + 32 * e;
-        const float macc = e ? x1 : x0;
-        a.m_out[gi] = full_band ? 0.0f : macc - (e ? l1 : l0);
-        if (kSgd) a.p_out[gi] = a.p_in[gi] - a.sgd.lr * (e ? q1 : q0);
+        const uint64_t gi = g0 + (e ? 63 - lane : lane);
+        const float macc = e ? xr : x0;
+        a.m_out[gi] = full_band ? 0.0f : macc - (e ? le - lo : le + lo);
+        if (kSgd) a.p_out[gi] = st_p[e] - a.sgd.lr * (e ? qe - qo : qe + qo);
       }
       continue;
     }
     // D = IDCT(W), W = wire - coef on the selection (k = s: W = wire, D = Q)
-    const float wd0 = full_band ? w0 : (sel0 ? w0 - c0f : 0.0f);
-    const float wd1 = full_band ? w1 : (sel1 ? w1 - c1f : 0.0f);
-    float d0 = 0.0f, d1 = 0.0f;
-    for (int e = 0; e < 2; ++e) {
-      unsigned m = __ballot_sync(kFull, (e ? wd1 : wd0) != 0.0f);
-      while (m) {
-        const int l = __ffs(m) - 1;
-        m &= m - 1;
-        const int j = l + 32 * e;
-        const float wj = __shfl_sync(kFull, e ? wd1 : wd0, l);
-        d0 = fmaf(wj, b32[j * S + lane], d0);
-        d1 = fmaf(wj, b32[j * S + lane + 32], d1);
-      }
+    wv[lane] = full_band ? w0 : (sel0 ? w0 - c0f : 0.0f);
+    wv[lane + 32] = full_band ? w1 : (sel1 ? w1 - c1f : 0.0f);
+    __syncwarp();
+    float de0 = 0.0f, do0 = 0.0f, de1 = 0.0f, do1 = 0.0f;
+    const float4* w4 = reinterpret_cast<const float4*>(wv);
+#pragma unroll 4
+    for (int q = 0; q < S / 4; q += 2) {
+      const float* b = b32 + 4 * q * S + lane;
+      const float4 w = w4[q], u = w4[q + 1];
+      de0 = fmaf(w.x, b[0], de0);
+      do0 = fmaf(w.y, b[S], do0);
+      de1 = fmaf(w.z, b[2 * S], de1);
+      do1 = fmaf(w.w, b[3 * S], do1);
+      de0 = fmaf(u.x, b[4 * S], de0);
+      do0 = fmaf(u.y, b[5 * S], do0);
+      de1 = fmaf(u.z, b[6 * S], de1);
+      do1 = fmaf(u.w, b[7 * S], do1);
     }
+    const float de = de0 + de1, dod = do0 + do1;
     const AdamScalars A = a.adam;
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-      const uint64_t gi = g0 + lane + 32 * e;
-      const float d = e ? d1 : d0;
-      const float gp = full_band ? d : (e ? x1 : x0) + d;  // g - local_q + Q (optim.cpp:65)
-      const float m1 = A.beta1 * a.ea_in[gi] + A.one_minus_beta1 * gp;
-      const float m2 = A.beta2 * a.es_in[gi] + A.one_minus_beta2 * gp * gp;
-      float pn = a.p_in[gi] - A.lr * adam_ratio(m1, m2, A);
+      const uint64_t gi = g0 + (e ? 63 - lane : lane);
+      const float d = e ? de - dod : de + dod;
+      const float gp = full_band ? d : (e ? xr : x0) + d;  // g - local_q + Q (optim.cpp:65)
+      const float m1 = A.beta1 * st_m1[e] + A.one_minus_beta1 * gp;
+      const float m2 = A.beta2 * st_m2[e] + A.one_minus_beta2 * gp * gp;
+      float pn = st_p[e] - A.lr * adam_ratio(m1, m2, A);
       pn -= A.lr_wd * pn;
       a.ea_out[gi] = m1;
       a.es_out[gi] = m2;

@@ -11,6 +11,9 @@ apply 2 front start, 3 front end (X in TMEM), 16 / 17 m_acc ring write start / e
 10 apply wait start, 11 inverse done, 12 state staged, 13 apply done; MMA 18 X in TMEM, 19 C of
 t-1 read (forward issued), 14 W ready, 15 D of t-1 read (inverse issued).  Prints, per tile, each stamp relative to tile 0's
 select start (us) and the tile period, then the mean of every gap over tiles 8..31.
+
+With --plain the normal library runs the mode --reps times (no stamps): the per-tile period at
+full speed, and a single-mode command for ncu (`ncu --set full -k regex:demo_tc_adam -s 2 -c 1`).
 """
 from __future__ import annotations
 
@@ -21,7 +24,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("DMB_LIB", os.path.join(ROOT, "paper_2502_06728_b200", "libdemo_b200_events.so"))
+if "--plain" not in sys.argv:
+    os.environ.setdefault("DMB_LIB", os.path.join(ROOT, "paper_2502_06728_b200", "libdemo_b200_events.so"))
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -44,9 +48,12 @@ def main():
     ap.add_argument("--k", type=int, default=32)
     ap.add_argument("--R", type=int, default=4)
     ap.add_argument("--sign", type=int, default=1, help="1: sign-mode payloads (MASK_SIGN), 0: fp32 values (MASK)")
+    ap.add_argument("--plain", action="store_true", help="time the mode with the normal library, no stamps")
+    ap.add_argument("--reps", type=int, default=5)
     a = ap.parse_args()
     lib = _capi.lib
-    lib.dmb_debug_events.argtypes = [C.c_void_p]
+    if not a.plain:
+        lib.dmb_debug_events.argtypes = [C.c_void_p]
     dev = torch.device("cuda", 0)
     sms = torch.cuda.get_device_properties(0).multi_processor_count
     L = sms * a.tiles_per_cta * 8192
@@ -113,6 +120,18 @@ def main():
 
     run()  # warm
     torch.cuda.synchronize()
+    if a.plain:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.reps):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        P.status()
+        ms = e0.elapsed_time(e1) / a.reps
+        print(f"mode {a.mode} (k {a.k}, sign {a.sign}, R {a.R}, plain): L = {L}, {ms:.3f} ms per launch sequence, "
+              f"{ms * 1e3 / a.tiles_per_cta:.2f} us per tile per CTA")
+        return
     lib.dmb_debug_events(C.c_void_p(buf.data_ptr()))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
