@@ -1658,9 +1658,12 @@ teardown:
 // AdamW as in the main kernel (whose apply warps left this chunk's state untouched); the
 // inverse uses the same symmetry: lane l computes D_l and D_{63-l} from the even and odd j.
 constexpr int kFixWarps = 8;
-// B row-major, B^T, then x per warp (FP64, or FP32 in the FMA pass); the rare FP64 pass
-// reads the FP64 basis through L1
-constexpr uint32_t FIX_SMEM = S * S * 4 + S * S * 4 + kFixWarps * S * 8;
+// the FP32 basis packed for 128-bit lane reads (forward: lane l's {B[l][i], B[l+32][i],
+// B[l][i+1], B[l+32][i+1]}, i even < 32; inverse: {B[4q..4q+3][l]}, l < 32), then 64 doubles
+// per warp (x in FP64, the folded x or the W rows in FP32); the rare FP64 pass reads the FP64
+// basis through L1
+constexpr uint32_t FIX_BASIS = 16 * 32 * 16;
+constexpr uint32_t FIX_SMEM = 2 * FIX_BASIS + kFixWarps * S * 8;
 // 9u bound above, with margin
 constexpr float kFmaEps = 14.0f * 5.9604645e-8f * 0.17677669f;
 
@@ -1688,20 +1691,22 @@ __device__ __forceinline__ void bitonic64_desc(uint32_t& v0, uint32_t& v1) {
 }
 
 template <ChunkMode MODE, int WIRE>
-__global__ void __launch_bounds__(kFixWarps * 32, 6) demo_fix64_kernel(const ChunkArgs a) {
+__global__ void __launch_bounds__(kFixWarps * 32, 4) demo_fix64_kernel(const ChunkArgs a) {
   constexpr bool kEncodeOnly = MODE == ChunkMode::EncodeAdam;
   constexpr bool kSgd = MODE == ChunkMode::StepSgd;
   constexpr bool kMomentum = kSgd || MODE == ChunkMode::EncodeSgd;
   extern __shared__ __align__(16) uint8_t fsm[];
-  float* b32 = reinterpret_cast<float*>(fsm);              // B[j][i] row-major
-  float* bt = reinterpret_cast<float*>(fsm + S * S * 4);    // B^T: (i, j) at i*64 + j
-  double* xw = reinterpret_cast<double*>(fsm + S * S * 8) + (threadIdx.x >> 5) * S;  // this warp's chunk
+  float4* bf4 = reinterpret_cast<float4*>(fsm);              // forward, [i / 2][l]
+  float4* bi4 = reinterpret_cast<float4*>(fsm + FIX_BASIS);  // inverse, [q][l]
+  double* xw = reinterpret_cast<double*>(fsm + 2 * FIX_BASIS) + (threadIdx.x >> 5) * S;  // this warp's chunk
   float* xf = reinterpret_cast<float*>(xw);
   if (*a.fb_count <= blockIdx.x * kFixWarps) return;  // no listed chunk for this CTA: skip the basis load
   if (!kEncodeOnly && step_failed(a.status)) return;
-  for (int u = 4 * threadIdx.x; u < S * S; u += 4 * blockDim.x) {
-    *reinterpret_cast<float4*>(b32 + u) = __ldg(reinterpret_cast<const float4*>(a.basis.B + u));
-    *reinterpret_cast<float4*>(bt + u) = __ldg(reinterpret_cast<const float4*>(a.basis.BT + u));
+  for (int u = threadIdx.x; u < 16 * 32; u += blockDim.x) {
+    const int l = u & 31, h = u >> 5;
+    const float* B = a.basis.B;  // B[j][i] at j * 64 + i
+    bf4[u] = make_float4(B[l * S + 2 * h], B[(l + 32) * S + 2 * h], B[l * S + 2 * h + 1], B[(l + 32) * S + 2 * h + 1]);
+    bi4[u] = make_float4(B[4 * h * S + l], B[(4 * h + 1) * S + l], B[(4 * h + 2) * S + l], B[(4 * h + 3) * S + l]);
   }
   __syncthreads();
   const bool need_signs = a.geo.sign_mode || a.geo.dtype == DMB_TERNARY;
@@ -1756,16 +1761,16 @@ __global__ void __launch_bounds__(kFixWarps * 32, 6) demo_fix64_kernel(const Chu
 #pragma unroll
       for (int q = 0; q < S / 8; ++q) {
         const float4 v = y4[q];
-        const float* r = bt + 4 * q * S;
+        const float4 r = bf4[(2 * q) * 32 + lane], t = bf4[(2 * q + 1) * 32 + lane];
         const int e = (4 * q) & 7;
-        s0[e] = fmaf(r[lane], v.x, s0[e]);
-        s1[e] = fmaf(r[lane + 32], v.x, s1[e]);
-        s0[e + 1] = fmaf(r[S + lane], v.y, s0[e + 1]);
-        s1[e + 1] = fmaf(r[S + lane + 32], v.y, s1[e + 1]);
-        s0[e + 2] = fmaf(r[2 * S + lane], v.z, s0[e + 2]);
-        s1[e + 2] = fmaf(r[2 * S + lane + 32], v.z, s1[e + 2]);
-        s0[e + 3] = fmaf(r[3 * S + lane], v.w, s0[e + 3]);
-        s1[e + 3] = fmaf(r[3 * S + lane + 32], v.w, s1[e + 3]);
+        s0[e] = fmaf(r.x, v.x, s0[e]);
+        s1[e] = fmaf(r.y, v.x, s1[e]);
+        s0[e + 1] = fmaf(r.z, v.y, s0[e + 1]);
+        s1[e + 1] = fmaf(r.w, v.y, s1[e + 1]);
+        s0[e + 2] = fmaf(t.x, v.z, s0[e + 2]);
+        s1[e + 2] = fmaf(t.y, v.z, s1[e + 2]);
+        s0[e + 3] = fmaf(t.z, v.w, s0[e + 3]);
+        s1[e + 3] = fmaf(t.w, v.w, s1[e + 3]);
       }
       const float f0 = ((s0[0] + s0[1]) + (s0[2] + s0[3])) + ((s0[4] + s0[5]) + (s0[6] + s0[7]));
       const float f1 = ((s1[0] + s1[1]) + (s1[2] + s1[3])) + ((s1[4] + s1[5]) + (s1[6] + s1[7]));
@@ -1908,18 +1913,18 @@ __global__ void __launch_bounds__(kFixWarps * 32, 6) demo_fix64_kernel(const Chu
       const float4* q4 = reinterpret_cast<const float4*>(wv + 64);
 #pragma unroll 4
       for (int q = 0; q < S / 4; ++q) {
-        const float* b = b32 + 4 * q * S + lane;
+        const float4 b = bi4[q * 32 + lane];
         const float4 c = l4[q];
-        le = fmaf(c.x, b[0], le);
-        lo = fmaf(c.y, b[S], lo);
-        le = fmaf(c.z, b[2 * S], le);
-        lo = fmaf(c.w, b[3 * S], lo);
+        le = fmaf(c.x, b.x, le);
+        lo = fmaf(c.y, b.y, lo);
+        le = fmaf(c.z, b.z, le);
+        lo = fmaf(c.w, b.w, lo);
         if (kSgd) {
           const float4 w = q4[q];
-          qe = fmaf(w.x, b[0], qe);
-          qo = fmaf(w.y, b[S], qo);
-          qe = fmaf(w.z, b[2 * S], qe);
-          qo = fmaf(w.w, b[3 * S], qo);
+          qe = fmaf(w.x, b.x, qe);
+          qo = fmaf(w.y, b.y, qo);
+          qe = fmaf(w.z, b.z, qe);
+          qo = fmaf(w.w, b.w, qo);
         }
       }
 #pragma unroll
@@ -1939,16 +1944,16 @@ __global__ void __launch_bounds__(kFixWarps * 32, 6) demo_fix64_kernel(const Chu
     const float4* w4 = reinterpret_cast<const float4*>(wv);
 #pragma unroll 4
     for (int q = 0; q < S / 4; q += 2) {
-      const float* b = b32 + 4 * q * S + lane;
+      const float4 b = bi4[q * 32 + lane], b2 = bi4[(q + 1) * 32 + lane];
       const float4 w = w4[q], u = w4[q + 1];
-      de0 = fmaf(w.x, b[0], de0);
-      do0 = fmaf(w.y, b[S], do0);
-      de1 = fmaf(w.z, b[2 * S], de1);
-      do1 = fmaf(w.w, b[3 * S], do1);
-      de0 = fmaf(u.x, b[4 * S], de0);
-      do0 = fmaf(u.y, b[5 * S], do0);
-      de1 = fmaf(u.z, b[6 * S], de1);
-      do1 = fmaf(u.w, b[7 * S], do1);
+      de0 = fmaf(w.x, b.x, de0);
+      do0 = fmaf(w.y, b.y, do0);
+      de1 = fmaf(w.z, b.z, de1);
+      do1 = fmaf(w.w, b.w, do1);
+      de0 = fmaf(u.x, b2.x, de0);
+      do0 = fmaf(u.y, b2.y, do0);
+      de1 = fmaf(u.z, b2.z, de1);
+      do1 = fmaf(u.w, b2.w, do1);
     }
     const float de = de0 + de1, dod = do0 + do1;
     const AdamScalars A = a.adam;
