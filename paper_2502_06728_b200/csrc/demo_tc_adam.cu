@@ -1406,11 +1406,14 @@ __global__ void __maxnreg__(128)
               prefetched = has_next;
               if (has_next) stage_rows(stg, t1 * TM + base);
             }
-            const int Rm = a.in.R;
+            // element e: accumulator e & 3, byte e >> 2, holding (sum of codes) + R; one PRMT
+            // puts the byte under the exponent of 2^23 and one FADD takes 2^23 + R off, exactly
+            // (an inactive row read zero words: every field counted 1 per member, so it gives 0)
+            const float bias = 8388608.0f + (float)a.in.R;
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {  // element e: accumulator e & 3, byte e >> 2
-              gq0[e] = act0 ? (float)((int)((a0[e & 3] >> (8 * (e >> 2))) & 0xffu) - Rm) : 0.0f;
-              gq1[e] = act1 ? (float)((int)((a1[e & 3] >> (8 * (e >> 2))) & 0xffu) - Rm) : 0.0f;
+            for (int e = 0; e < 16; ++e) {
+              gq0[e] = __uint_as_float(__byte_perm(a0[e & 3], 0x4B000000u, 0x7650u + (e >> 2))) - bias;
+              gq1[e] = __uint_as_float(__byte_perm(a1[e & 3], 0x4B000000u, 0x7650u + (e >> 2))) - bias;
             }
             sel0 = act0 ? gather16(om0, s) : 0u;
             sel1 = act1 ? gather16(om1, s) : 0u;
