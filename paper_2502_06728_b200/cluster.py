@@ -42,6 +42,7 @@ Environment switches (measurement and fallbacks; the defaults are the measured b
   DMB_OVERLAP=1        overlapped merges on split SMs (DMB_MERGE_SMS: the merges' share)
   DMB_PULL_FUSED=0     pulled reduce-scatter as a mean pass even for AdamW
   DMB_PULL_STAGED=1    stage the peers' slices by copy engines for the one-pass step too
+  DMB_CE_PEER_STREAMS=1  pull the peers' slices on one copy stream per peer (measured slower)
 
 The exchange is injectable: `CollectiveExchange` (torch.distributed all-gather, any
 backend), `CopyEngineExchange` (symmetric memory pulled by copy engines over NVLink, NCCL
@@ -771,6 +772,11 @@ class HybridCluster:
                         for a in range(A) if a != self.accel}
         self._pull_stream = torch.cuda.Stream(self.device)  # the member-order means
         self._copy_stream = torch.cuda.Stream(self.device)  # the copy-engine pulls, a bucket ahead of the means
+        # opt-in (DMB_CE_PEER_STREAMS=1): one stream per peer, so the copies from several peers
+        # (A > 2) run on several copy engines at once -- bit-identical, but measured slower at 4x1
+        # (AdamW 16.1 ms against 12.1 ms on one stream: the concurrent pulls contend)
+        self._peer_streams = ({a: torch.cuda.Stream(self.device) for a in self._gstage}
+                              if os.environ.get("DMB_CE_PEER_STREAMS", "0") == "1" and len(self._gstage) > 1 else {})
         self._pull_ctas = int(ctas)
         self._pulled = None
         self._pull_fused = False
@@ -817,6 +823,22 @@ class HybridCluster:
                 ev = torch.cuda.Event()
                 ev.record(self._copy_stream)
                 copied = [ev] * len(spans)
+            elif self._peer_streams:
+                opened = torch.cuda.Event()
+                opened.record(self._copy_stream)  # after the barrier
+                for ps in self._peer_streams.values():
+                    ps.wait_event(opened)
+                for lo, hi in spans:
+                    for a, stg in self._gstage.items():
+                        with torch.cuda.stream(self._peer_streams[a]):
+                            stg[lo:hi].copy_(views[a][off0 + lo:off0 + hi], non_blocking=True)
+                    for ps in self._peer_streams.values():  # the bucket's copies from every peer
+                        e = torch.cuda.Event()
+                        e.record(ps)
+                        self._copy_stream.wait_event(e)
+                    ev = torch.cuda.Event()
+                    ev.record(self._copy_stream)
+                    copied.append(ev)
             else:
                 for lo, hi in spans:
                     for a, stg in self._gstage.items():

@@ -9,8 +9,9 @@
    inputs (cluster.cpp:193-231): prepare per member, decode_and_merge in member order, apply;
 3. a non-finite gradient on the last rank refuses the step on every rank (TrainingError) and
    leaves every state vector bit-identical, in the pipelined and in the windowed mode;
-4. with shard groups of two (2 x N/2), the reduce-scatter pulled over NVLink from symmetric
-   memory gives the NCCL reduce-scatter's results bit for bit, and refuses a NaN step.
+4. with shard groups of two and of four (2 x N/2, 4 x N/4), the reduce-scatter pulled over
+   NVLink from symmetric memory gives the NCCL reduce-scatter's results bit for bit, and refuses
+   a NaN step.
 Rank 0 prints one JSON line with the outcome; the exit code is non-zero on any failure.
 """
 from __future__ import annotations
@@ -139,10 +140,12 @@ def main():
                 worst = max(worst, float(err))
         out[f"{opt_kind}_oracle_max_err"] = worst
         ok &= worst <= 1e-5 if opt_kind == "sgd" else worst <= 1e-5
-    # 4. S = 2 (shard groups of two): the pulled reduce-scatter (symmetric memory, NVLink) against
+    # 4. S = 2 and 4 (shard groups of two, four): the pulled reduce-scatter (symmetric memory, NVLink) against
     #    NCCL's, bit-identical over two steps, and a refused step with the pull
-    if world % 2 == 0:
-        topo2 = Topology(nodes=world // 2, accels_per_node=2)
+    for S in (2, 4):
+        if world % S:
+            continue
+        topo2 = Topology(nodes=world // S, accels_per_node=S)
         sg2, rg2 = groups_for(topo2, rank)
         for opt_kind in ("sgd", "adamw"):
             opt = P.OptimizerConfig(P.OptimizerKind.DemoSgd if opt_kind == "sgd" else P.OptimizerKind.DecoupledAdamW,
@@ -150,11 +153,16 @@ def main():
             cfg = P.ReplicatorConfig(P.Scheme.DeMo, 64, 32, 0.5, True, P.TransferDtype.Fp32, 1234)
             p0 = torch.empty(L, device=dev).normal_(0, 0.02, generator=torch.Generator(device=dev).manual_seed(7))
             res = {}
-            for pull in (False, True):
+            # S = 4: NCCL's ring sums four members in its own order, so only the pulls (member order,
+            # mean_of) are compared bit for bit -- one copy stream against one per peer -- and NCCL within 1e-5
+            variants = (False, True) if S == 2 else (False, True, "single")
+            for pull in variants:
                 os.environ["DMB_CE_GATHER"] = "1"
                 os.environ.pop("DMB_GATHER_BUDGET", None)
-                cl = HybridCluster(topo2, L, opt, cfg, p0, rank, sg2, rg2, buckets=8, wire="mask", pull_grads=pull)
-                padded = cl.spec.extent * 2
+                os.environ["DMB_CE_PEER_STREAMS"] = "0" if pull == "single" else "1"  # both copy schedules
+                cl = HybridCluster(topo2, L, opt, cfg, p0, rank, sg2, rg2, buckets=8, wire="mask",
+                                   pull_grads=bool(pull))
+                padded = cl.spec.extent * S
                 for step in range(2):
                     g = torch.empty(padded, device=dev).normal_(
                         0, 1e-3, generator=torch.Generator(device=dev).manual_seed(100 * step + rank))
@@ -164,7 +172,7 @@ def main():
                     cl.step(step, 0.01, g)
                 res[pull] = [cl.params.clone()] + ([cl.m.clone()] if opt_kind == "sgd" else
                                                    [cl.exp_avg.clone(), cl.exp_avg_sq.clone()])
-                if pull:  # a NaN in one member's gradient refuses the step on every rank
+                if pull is True:  # a NaN in one member's gradient refuses the step on every rank
                     keep = [t.clone() for t in res[pull]]
                     gb = cl.grad_buffer(2)
                     gb.normal_(0, 1e-3, generator=torch.Generator(device=dev).manual_seed(300 + rank))
@@ -177,11 +185,20 @@ def main():
                         refused = True
                     now = [cl.params] + ([cl.m] if opt_kind == "sgd" else [cl.exp_avg, cl.exp_avg_sq])
                     untouched = all(torch.equal(a, b) for a, b in zip(keep, now))
-                    out[f"{opt_kind}_2xR_pull_refused"] = refused and untouched
+                    out[f"{opt_kind}_{S}xR_pull_refused"] = refused and untouched
                     ok &= refused and untouched
-            same = all(torch.equal(a, b) for a, b in zip(res[False], res[True]))
-            out[f"{opt_kind}_2xR_pull_vs_nccl_bit_identical"] = same
-            ok &= same
+            if S == 2:
+                same = all(torch.equal(a, b) for a, b in zip(res[False], res[True]))
+                out[f"{opt_kind}_{S}xR_pull_vs_nccl_bit_identical"] = same
+                ok &= same
+            else:
+                same = all(torch.equal(a, b) for a, b in zip(res["single"], res[True]))
+                out[f"{opt_kind}_{S}xR_pull_peer_streams_vs_one_stream_bit_identical"] = same
+                rel = max(float(((a - b).abs().max() / b.abs().max().clamp_min(1e-30)).item())
+                          for a, b in zip(res[False], res[True]))
+                out[f"{opt_kind}_{S}xR_pull_vs_nccl_max_rel"] = rel
+                ok &= same and rel <= 1e-5
+            os.environ.pop("DMB_CE_PEER_STREAMS", None)
     t = torch.tensor([0 if ok else 1], device=dev)
     dist.all_reduce(t)
     out["ok"] = int(t.item()) == 0
