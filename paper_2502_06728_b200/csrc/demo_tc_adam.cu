@@ -1560,6 +1560,14 @@ __global__ void __maxnreg__(128)
         const bool w1_all = kSgd && WIRE == kWireF32;
         const uint32_t cs0 = (full_band && !w1_all) || kMergeSgd ? 0u : sel0;  // coef on the selection
         const uint32_t cs1 = (full_band && !w1_all) || kMergeSgd ? 0u : sel1;
+        if (kMerge && !a.geo.wire_mask) {  // reference-layout bodies: the grid rows from the scratch
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int col = qcol(e, s);
+            gq0[e] = grid[l0 * S + (col ^ ((l0 & 7) << 3))];
+            gq1[e] = grid[l1 * S + (col ^ ((l1 & 7) << 3))];
+          }
+        }
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int col = qcol(e, s);
@@ -1578,11 +1586,9 @@ __global__ void __maxnreg__(128)
               u1[e] = __uint_as_float(__float_as_uint(wire_of<WIRE>(c1[e])) & m1);
             }
           } else if (kMerge) {  // an inactive row has no selection and an empty grid row
-            const float g0v = a.geo.wire_mask ? gq0[e] : grid[l0 * S + (col ^ ((l0 & 7) << 3))];
-            const float g1v = a.geo.wire_mask ? gq1[e] : grid[l1 * S + (col ^ ((l1 & 7) << 3))];
             // MergeAdam: W = Q - local_q of the own selection; MergeSgd: W = grid / R (Q)
-            v0 = g0v * invR - __uint_as_float(b0 & k0);
-            v1 = g1v * invR - __uint_as_float(b1 & k1);
+            v0 = gq0[e] * invR - __uint_as_float(b0 & k0);
+            v1 = gq1[e] * invR - __uint_as_float(b1 & k1);
           } else {
             // W = wire - coef on the selection (k = s: W = wire)
             v0 = __uint_as_float(__float_as_uint(wire_of<WIRE>(c0[e]) - __uint_as_float(b0 & k0)) & m0);
