@@ -1388,9 +1388,12 @@ __global__ void __maxnreg__(128)
                 v0 = act0 ? __ldg(dv + 4 * r0 + s) : 0u;
                 v1 = act1 ? __ldg(dv + 4 * r1 + s) : 0u;
               }
-              if (s < 2 && (s ? act1 : act0)) {
+              if (staged) {  // branch-free: lanes 2-3 of a quad read lanes 0-1's masks (a broadcast)
+                const bool chk = s < 2 && ((s & 1) ? act1 : act0);
+                bad |= chk && __popcll(smk[rr * 16 + q0 + 8 * (s & 1)]) != k;
+              } else if (s < 2 && (s ? act1 : act0)) {
                 const unsigned long long* mk = reinterpret_cast<const unsigned long long*>(a.in.body[rr]);
-                bad |= __popcll(staged ? smk[rr * 16 + q0 + 8 * s] : __ldg(mk + (s ? r1 : r0))) != k;
+                bad |= __popcll(__ldg(mk + (s ? r1 : r0))) != k;
               }
               bad |= (((v0 & (v0 >> 1)) | (v1 & (v1 >> 1))) & H) != 0u;
               const uint32_t t0 = (v0 & H) + (~(v0 >> 1) & H), t1v = (v1 & H) + (~(v1 >> 1) & H);
