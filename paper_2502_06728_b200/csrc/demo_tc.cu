@@ -20,7 +20,7 @@
 // replicate.cpp:137-144 + :282-309 (conditioning, merge), optim.cpp:18-74.
 //
 // Certification bound: |c~_j - c_j| <= kEpsScale * ||x||_1, derived with the per-MMA model
-// of demo_tc_adam.cu (kEpsScale there): one tcgen05.mma kind::tf32 step (K = 8) takes exact
+// of demo_tc_adam.cu (at kEpsW / kEpsL there): one tcgen05.mma kind::tf32 step (K = 8) takes exact
 // products, aligns every term to the largest exponent with truncation and truncates the sum
 // once -> error <= 9 * 2^-23 (|acc| + sum |terms|).  With S = sum_i |x_i||B_ji| <=
 // sqrt(2/s) ||x||_1 and RNA TF32 splits (|x - hi| <= 2^-11 |x|, |x - hi - lo| <= 2^-22 |x|,

@@ -96,17 +96,26 @@ __host__ __device__ constexpr uint32_t col_macc(bool q2) { return q2 ? 384u : 25
 constexpr uint32_t OFF_M = OFF_SCR;  // SGD modes: the momentum tile of the gradient split
 constexpr uint32_t TMEM_COLS = 512;
 
-// Certification radius of a tensor-core coefficient: |c_tc - c_oracle| <= kEpsScale ||x||_1.
+// Certification radius of a tensor-core coefficient, per chunk:
+//   |c_tc - c_oracle| <= eps = kEpsW Lw + kEpsL ||x||_1,  Lw = sum_i (8 - floor(i / 8)) |x_i|.
 // Model of one tcgen05.mma kind::tf32 step (K = 8): exact products, every term aligned to the
 // largest exponent and truncated, the sum truncated once -> error <= 9 * 2^-23 (|acc| +
-// sum |terms|).  With S = sum_i |x_i||B_ji| <= sqrt(2/s) ||x||_1:
-//   8 hi*hi steps last:        8 * 9 * 2^-23 * (1 + 2^-9) S            = 8.60e-6 S
+// sum |terms|).  With S_u = sum_{i in K-step u} |x_i||B_ji| <= sqrt(2/s) L_u (L_u the |x| sum
+// of the step's eight elements, TMEM column = element) and S = sum_u S_u:
+//   8 hi*hi steps last, u = 1..8 in element order: step u sees |acc| <= S_1 + .. + S_{u-1} +
+//   2^-9 S (the cross terms before), so the sum is 9 * 2^-23 (sum_u (9 - u) S_u + 8 * 2^-9 S)
+//                               <= 9 * 2^-23 sqrt(2/s) (Lw + 2^-6 ||x||_1)
+//   (all weights 8 gives the uniform bound 8 * 9 * 2^-23 (1 + 2^-9) S = 8.60e-6 S; a Gaussian
+//   chunk has Lw ~ 4.5 ||x||_1)
 //   16 cross-term steps first:  16 * 9 * 2^-23 * 1.5 * 2^-10 S          = 2.5e-8 S
 //   split residuals (x: hi = top 10 mantissa bits, lo read as TF32; B: RNA hi/lo):
 //                               (2^-22 + 2^-20 + 2^-21) S              = 1.67e-6 S
 //   oracle's own FP64 rounding: 64 * 2^-53 S                            ~ 0
-// total 1.03e-5 S; 1.05e-5 sqrt(2/64) ||x||_1 is used.
-constexpr float kEpsScale = 1.05e-05f * 0.1767766952966369f;
+// with S <= sqrt(2/64) ||x||_1: Lw carries 9 * 2^-23 = 1.073e-6 (1.10e-6 used), ||x||_1 carries
+// 1.68e-8 + 2.5e-8 + 1.669e-6 = 1.711e-6 (1.75e-6 used), both times sqrt(2/64).  The front
+// sums Lw and ||x||_1 in FP32 (relative error <= 64 u, inside the margins).
+constexpr float kEpsW = 1.10e-06f * 0.1767766952966369f;
+constexpr float kEpsL = 1.75e-06f * 0.1767766952966369f;
 
 __device__ __forceinline__ uint32_t sw_off(int r, int q) {  // 16-byte unit q of row r
   return (uint32_t)(q >> 3) * (TM * 128u) + (uint32_t)r * 128u + ((uint32_t)((q & 7) ^ (r & 7)) << 4);
@@ -579,7 +588,7 @@ __global__ void __maxnreg__(128)
   uint64_t* bar_s = bar_i + 1;  // [2] optimizer state staged, per 32-column half (TMA)
   uint64_t* bar_a = bar_s + 2;  // [2] that half written back into the staging tile (apply warps)
   uint64_t* bar_c = bar_a + 2;  // coefficient tile read out of TMEM (select warps)
-  uint64_t* bar_l = bar_c + 1;  // [2] ||x||_1 of tile n in l1buf[n & 1] (apply warps)
+  uint64_t* bar_l = bar_c + 1;  // [2] the radii of tile n in l1buf[n & 1] (apply warps)
   uint64_t* bar_p = bar_l + 2;  // [2] MASK_SIGN encode: selection pieces of tile n in buffer n & 1 (select)
   uint64_t* bar_q = bar_p + 2;  // [2] ... and that buffer written out as the payload (apply warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_q + 2);
@@ -714,7 +723,7 @@ __global__ void __maxnreg__(128)
     // D = A(TMEM: hi, lo) x B(smem hi, lo) in 3xTF32 over K = 64.  The 16 small
     // cross terms (hi*lo, lo*hi: |term| <= 2^-10 |x||B|) accumulate first and the 8 hi*hi
     // steps last, so the accumulator is small while the small terms are added: this is
-    // what the certification radius kEpsScale assumes (see there).
+    // what the certification radius (kEpsW, kEpsL) assumes (see there).
     auto issue = [&](uint32_t d, uint32_t bh, uint32_t bl, uint64_t* bar, uint32_t ah = COL_XH,
                      uint32_t al = COL_XL) {
       tc_fence_after();
@@ -789,7 +798,7 @@ __global__ void __maxnreg__(128)
     auto front = [&](uint64_t t, uint32_t n, int part) {
       evt(a, tid == 32 * kSelWarps, n, part == kRing ? 16 : 2);
       if (part != kRing) mbar_wait(bar_g, n & 1);
-      float l1 = 0.f;
+      float l1 = 0.f, lw = 0.f;  // ||x||_1 and the K-step-weighted sum of the radius
       bool fin = true;
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
@@ -843,7 +852,10 @@ __global__ void __maxnreg__(128)
         if (kMomentum && part != kSplit) tmem_st16(tmem + tl + COL_MACC + 64 * (n & 1) + 16 * h, x);  // m_acc
         if (part == kRing) continue;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) l1 += fabsf(x[e]);
+        for (int e = 0; e < 16; ++e) {
+          l1 += fabsf(x[e]);
+          lw = fmaf((float)(8 - ((16 * h + e) >> 3)), fabsf(x[e]), lw);  // K-step weight of element 16h + e
+        }
         if (!kMomentum && !kEncodeOnly) tmem_st16(tmem + tl + COL_G + 64 * (n % 3) + 16 * h, x);  // raw g
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
@@ -869,7 +881,7 @@ __global__ void __maxnreg__(128)
         }
         (void)gs;
       }
-      l1buf[(n & 1) * TM + trow] = l1;
+      l1buf[(n & 1) * TM + trow] = kEpsW * lw + kEpsL * l1;  // the chunk's certification radius
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -1258,7 +1270,7 @@ __global__ void __maxnreg__(128)
             if (!have_kth) kth = quad_min(kq);
             if (!have_nxt) nxt = quad_max(nq);
           }
-          const float eps = kEpsScale * l1;
+          const float eps = l1;  // the radius the front computed (NaN for a non-finite chunk)
           const bool sel_unc = !full_band && !(kth - nxt > 2.0f * eps);
           const bool sign_unc = need_signs && !(kth > eps);
           return act && !isnan(l1) && (sel_unc || sign_unc || a.force_fp64);

@@ -427,7 +427,7 @@ def test_grad_mean_member_order(golden):
 # --------------------------------------------------------------- tensor-core path
 def test_tc_coefficient_error_within_certification_margin(oracle, monkeypatch):
     """The 3xTF32 tcgen05 DCT's coefficient error, measured against the FP64 oracle, stays
-    well inside the certification radius eps = 1.05e-5 sqrt(2/s) ||x||_1 the kernel assumes
+    well inside the certification radius eps = sqrt(2/s) (1.10e-6 Lw + 1.75e-6 ||x||_1) the kernel assumes
     (the bound derived in demo_tc_adam.cu from the per-MMA truncation model)."""
     p = P()
     monkeypatch.setenv("DMB_TC", "1")
@@ -438,10 +438,13 @@ def test_tc_coefficient_error_within_certification_margin(oracle, monkeypatch):
     enc = p.select_and_encode(dev(v), rep_to_cfg(rep), 0, 0)
     got = host(enc.update.values).reshape(-1, 64)
     want = oracle.select_and_encode(v.astype(np.float64), rep, 0, 0)["values"].reshape(-1, 64)
-    eps = 1.05e-5 * np.sqrt(2 / 64) * np.abs(v.astype(np.float64)).reshape(-1, 64).sum(axis=1)
+    ax = np.abs(v.astype(np.float64)).reshape(-1, 64)
+    lw = (ax * (8 - np.arange(64) // 8)).sum(axis=1)  # the K-step-weighted |x| sum of the hi*hi steps
+    eps = np.sqrt(2 / 64) * (1.10e-6 * lw + 1.75e-6 * ax.sum(axis=1))
     ratio = (np.abs(got - want).max(axis=1) / eps).max()
-    print(f"tensor-core coefficient error: max {ratio:.4g} of the certification radius 1.05e-5 sqrt(2/s) ||x||_1")
-    assert ratio < 0.25, f"tensor-core coefficient error reaches {ratio:.3f} of the certification radius"
+    print(f"tensor-core coefficient error: max {ratio:.4g} of the certification radius "
+          f"sqrt(2/s) (1.10e-6 Lw + 1.75e-6 ||x||_1)")
+    assert ratio < 0.5, f"tensor-core coefficient error reaches {ratio:.3f} of the certification radius"
 
 
 @pytest.mark.parametrize("k", [8, 32, 56])
