@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--buckets", type=int, default=None,
                     help="N>1: chunk-aligned buckets of the shard pipelined through prepare / all-gather / merge "
-                         "(default: 4 at S = 1, 8 at S > 1, where they also pipeline the reduce-scatter)")
+                         "(default: 4 at S = 1, 8 at S = 2, 16 at S >= 4; at S > 1 they also pipeline the reduce-scatter)")
     ap.add_argument("--wire", choices=["mask", "reference"], default="mask",
                     help="N>1 DeMo exchange layout: lossless u64-mask + packed values, or the reference body")
     ap.add_argument("--sm-reserve", type=int, default=0,
@@ -282,8 +282,8 @@ def run_ours(args, rank, world, local_rank):
         topo = Topology(nodes=R, accels_per_node=S)
         sg, rg = groups_for(topo, rank)
         os.environ["DMB_SM_RESERVE"] = str(args.sm_reserve)
-        if args.buckets is None:
-            args.buckets = 4 if S == 1 else 8
+        if args.buckets is None:  # measured best: 4x1 16-32 buckets (133 G) against 8 (118 G); 2x2 8
+            args.buckets = 4 if S == 1 else (8 if S == 2 else 16)
         cluster = HybridCluster(topo, L, opt, cfg, params, rank, sg, rg, buckets=args.buckets, wire=args.wire,
                                 pull_grads=bool(args.pull_rs) and S > 1, pull_ctas=args.pull_ctas)
         del params
